@@ -1,0 +1,204 @@
+/*
+ * dyq.h -- C ABI of the B200-native DyQ-VLA qlinear hot path (libdyq.so).
+ *
+ * The method (arXiv 2603.07904, /root/reference/PAPER.md = "P:line"): weights
+ * are frozen at INT4 ("INT4-pinned weights across all precision settings",
+ * P:332-333), activations are re-quantized every control step at a width
+ * b*_t in {2,4,8} or bypassed at BF16 (16), and b*_t is chosen
+ * from two kinematic proxies by the Eq. (6) lookup and the Alg. 1 hysteresis
+ * dispatcher.  This header exposes that hot path:
+ *
+ *   dyq_pack_weights   - offline weight quantization at wbits (Eq. 2)
+ *   dyq_select_bits    - kinematic proxies -> S_t -> bhat_t -> b*_t (Alg. 1)
+ *   dyq_act_quant      - dynamic activation quantization at the step's width
+ *   dyq_qlinear        - quantized linear layer  y = dequant(I)
+ *
+ * Conventions (all functions):
+ *  - Pointers are DEVICE pointers unless the parameter says "host".
+ *  - Every call is stream-ordered on `stream` and non-blocking: no host
+ *    synchronization, no device allocation.  The caller owns every buffer and
+ *    sizes them with the *_size / *_workspace queries.
+ *  - Returns dyq_status_t.  Argument / shape errors are detected synchronously
+ *    (DYQ_EINVAL / DYQ_ESHAPE / DYQ_EUNSUPPORTED) before anything is enqueued;
+ *    dyq_last_error() returns a thread-local message.  CUDA launch failures
+ *    return DYQ_ECUDA.  No C++ exception crosses this ABI.
+ *  - Non-finite inputs ("rejects input with a diagnostic identifying the
+ *    offending index") cannot be detected synchronously on a stream: kernels
+ *    atomicMin the smallest offending linear element index into the caller's
+ *    device int64 `err` (initialise it with dyq_error_reset; INT64_MAX = none)
+ *    and the caller polls it (dyq_error_read).  Outputs derived from
+ *    non-finite inputs are unspecified.  `err` may be NULL (no reporting).
+ *  - Packed weights are immutable after packing and may be shared by any
+ *    number of streams.  Selection state is single-owner and mutated in step
+ *    order.
+ *
+ * Layouts: see DESIGN.md §"Data layout in HBM".  Tensors are row-major.
+ * bf16 is passed as raw 16-bit patterns (uint16_t).
+ */
+#ifndef DYQ_H
+#define DYQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define DYQ_API __attribute__((visibility("default")))
+#else
+#define DYQ_API
+#endif
+
+typedef struct CUstream_st* dyq_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    DYQ_OK = 0,
+    DYQ_EINVAL = 1,       /* bad argument value (bits, null pointer, table ordering) */
+    DYQ_ESHAPE = 2,       /* inconsistent / unsupported shape (K % G, N % 16, ...)   */
+    DYQ_EUNSUPPORTED = 3, /* valid but not implemented on this build                */
+    DYQ_ENONFINITE = 4,   /* non-finite input (reported through err)               */
+    DYQ_ECUDA = 5,        /* CUDA runtime error                                     */
+    DYQ_ENCCL = 6         /* collective error                                       */
+} dyq_status_t;
+
+/* Thread-local description of the last error on this thread ("" if none). */
+DYQ_API const char* dyq_last_error(void);
+/* Library version string, e.g. "dyq 0.1 sm_100a". */
+DYQ_API const char* dyq_version(void);
+
+/* ---------------------------------------------------------------- errors */
+/* err: device int64; reset to INT64_MAX (= no error). */
+DYQ_API dyq_status_t dyq_error_reset(int64_t* err, dyq_stream_t stream);
+/* Synchronizes `stream` and copies *err to *host_index (INT64_MAX = none).
+ * Returns DYQ_ENONFINITE if an index was recorded.  (Debug / test path.) */
+DYQ_API dyq_status_t dyq_error_read(const int64_t* err, int64_t* host_index, dyq_stream_t stream);
+
+/* ------------------------------------------------------------ weight pack */
+/* Weight descriptor.  One (scale, zero-point) per output row n and per group
+ * of `group` consecutive input channels (reading 5).
+ *   N          output features (rows of W), N % 16 == 0
+ *   K          input features, K % group == 0
+ *   group      G in {64, 128}
+ *   wbits      4 (the paper's INT4-pinned weights) or 8 (optional table)
+ *   round_mode 0 = floor exactly as Eq. (2) (default), 1 = round-to-nearest  */
+typedef struct {
+    int32_t N, K, group, wbits, round_mode;
+} dyq_wdesc_t;
+
+/* Bytes of the packed code buffer and of the metadata buffer (scales fp32 +
+ * zero-points u8, 5 B per (row, group), padded to whole 128-row tiles). */
+DYQ_API dyq_status_t dyq_pack_weights_size(const dyq_wdesc_t* wd, size_t* codes_bytes,
+                                   size_t* meta_bytes);
+
+/* Quantize W [N,K] bf16 (device) per (row, group) with the fit of DESIGN.md
+ * readings 2-4 (zero-inclusive min-max in fp64, fp32 stored scale, half-up
+ * zero point) and Eq. (2); write codes in the kernel layout and
+ * the metadata.  codes / meta: device buffers of the sizes above (16-byte
+ * aligned).  Offline: not on the per-step path ("we freeze the weights"). */
+DYQ_API dyq_status_t dyq_pack_weights(const dyq_wdesc_t* wd, const uint16_t* w_bf16,
+                              void* codes, void* meta, int64_t* err,
+                              dyq_stream_t stream);
+
+/* Test hook: decode the kernel layout back to logical q [N,K] u8,
+ * s [N,K/G] fp32, z [N,K/G] u8 (device buffers). */
+DYQ_API dyq_status_t dyq_unpack_for_check(const dyq_wdesc_t* wd, const void* codes,
+                                  const void* meta, uint8_t* q, float* s,
+                                  uint8_t* z, dyq_stream_t stream);
+
+/* -------------------------------------------------------- bit selection */
+/* Calibration table; field names follow SPEC S:261 (CalibrationTable JSON).
+ *   theta_24, theta_48, theta_fp  Eq. (6) thresholds and the fallback
+ *                                 threshold, 0<=t24<=t48<=tfp
+ *   lambda                        fusion weight in [0,1]
+ *   D_acc, eta                    error-bound parameters, > 0
+ *                                 (calibration only; validated, unused here)
+ *   J_cap                         jerk cap (> 0; use 1e300 for none)
+ *   K                             Alg. 1 delay window, >= 1
+ *   W_macro, W_micro              window lengths, 1..64
+ *   H                             p95 history length, 1..1024
+ *   clamp_M                       1 = clamp M to [0,1], 0 = literal */
+typedef struct {
+    double theta_24, theta_48, theta_fp, lambda, D_acc, eta, J_cap;
+    int32_t K, W_macro, W_micro, H, clamp_M;
+} dyq_calib_t;
+
+/* Device bytes of the selection state for E control streams. */
+DYQ_API dyq_status_t dyq_state_size(int32_t E, const dyq_calib_t* calib, size_t* bytes);
+/* Initialise the state (all histories empty, dispatcher (16,0,16)). */
+DYQ_API dyq_status_t dyq_state_init(int32_t E, const dyq_calib_t* calib, void* state,
+                            dyq_stream_t stream);
+/* Episode reset for streams with mask[e] != 0 (mask: device u8 [E] or NULL =
+ * all): clears windows, prev_rot, warm-up and the dispatcher; keeps the p95
+ * history buffers (reading 23). */
+DYQ_API dyq_status_t dyq_state_reset_episode(void* state, const uint8_t* mask,
+                                     dyq_stream_t stream);
+/* One control step for every stream: observe a_{t-1} (prev_action, device
+ * float [E,7] = [x,y,z, rx,ry,rz, gripper], or NULL at t = 0), update the
+ * kinematic proxies M_t and J_t, the windowed means
+ * (P:229-231), S_t, bhat_t (Alg. 1 line 2) and b*_t (Alg. 1
+ * lines 3-9).  Writes bits[E] (int32 in {2,4,8,16}) and,
+ * optionally, S_out[E] (fp64) and target_out[E] (bhat_t).  Bit-exact with the
+ * CPU oracle (fp64, fixed evaluation order, no FMA contraction). */
+DYQ_API dyq_status_t dyq_select_bits(void* state, int32_t E, const float* prev_action,
+                             int32_t* bits, double* S_out, int32_t* target_out,
+                             dyq_stream_t stream);
+/* Expand per-episode bits to per-token activation bits through the variant
+ * table (DESIGN.md conflict C1): row_bits[m] = abits_of(bits[m / tokens_per_episode]).
+ * abits_of maps b* in {2,4,8,16} -> activation bits; pass NULL for identity
+ * (the paper's W4-pinned table: W4A2 / W4A4 / W4A8 / W4A16). */
+DYQ_API dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t tokens_per_episode,
+                            const int32_t* abits_of_host /* [4] or NULL */,
+                            int32_t* row_bits, dyq_stream_t stream);
+
+/* -------------------------------------------------- activation quantizer */
+/* Workspace bytes for dyq_qlinear with M tokens against descriptor wd (holds
+ * the quantized activations, their per-group parameters and the split-K
+ * partials).  Must be zeroed once before first use (dyq_workspace_init). */
+DYQ_API dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* bytes);
+DYQ_API dyq_status_t dyq_workspace_init(void* workspace, size_t bytes, dyq_stream_t stream);
+
+/* ------------------------------------------------------------- qlinear */
+/* y[m,n] = Sum_g s_x[m,g] s_w[n,g] Sum_{k in g} (Xq[m,k]-z_x[m,g]) (q[n,k]-z_w[n,g])
+ * for integer rows (row_bits[m] in {2,4,8}); the codes Xq are the dynamic
+ * quantization of x[m,:] at row_bits[m] bits (Eq. 2 per (token, group)).
+ * For A16 rows (row_bits[m] == 16, the BF16 bypass):
+ * y[m,n] = Sum_g s_w[n,g] Sum_{k in g} x[m,k] (q[n,k]-z_w[n,g]).
+ *   x         device bf16 [M,K]
+ *   row_bits  device int32 [M] (activation bits per token) or NULL -> `bits`
+ *   y         device [M,N], y_dtype 0 = fp32, 1 = bf16
+ *   workspace device buffer of dyq_qlinear_workspace() bytes (zeroed once)
+ * One call reads the packed weights once for any mix of activation widths.
+ * M in [0, 65536]; M <= 16 runs the bandwidth-bound decode kernel, larger M
+ * the tcgen05 prefill kernel.  Integer group sums are exact (int32); the fp32
+ * epilogue order is unspecified (tolerance in DESIGN.md). */
+DYQ_API dyq_status_t dyq_qlinear(const dyq_wdesc_t* wd, const void* codes, const void* meta,
+                         const uint16_t* x, int32_t M, const int32_t* row_bits,
+                         int32_t bits, void* y, int32_t y_dtype, void* workspace,
+                         size_t ws_bytes, int64_t* err, dyq_stream_t stream);
+
+/* Test hook: same main loop, writes the exact integer group sums
+ * I[m,n,g] (int32 [M,N,K/G]; 0 for A16 rows) instead of y. */
+DYQ_API dyq_status_t dyq_qlinear_i32_partials(const dyq_wdesc_t* wd, const void* codes,
+                                      const void* meta, const uint16_t* x, int32_t M,
+                                      const int32_t* row_bits, int32_t bits,
+                                      int32_t* I, void* workspace, size_t ws_bytes,
+                                      int64_t* err, dyq_stream_t stream);
+
+/* Test hook: run only the activation quantizer of dyq_qlinear and export its
+ * result in logical layout: xq [M,K] u8, sx [M,K/G] fp32, zx [M,K/G] u8,
+ * SX [M,K/G] int32 (A16 rows zeroed).  Same kernel as the qlinear path. */
+DYQ_API dyq_status_t dyq_act_quant_for_check(const dyq_wdesc_t* wd, const uint16_t* x, int32_t M,
+                                     const int32_t* row_bits, int32_t bits, uint8_t* xq,
+                                     float* sx, uint8_t* zx, int32_t* SX, void* workspace,
+                                     size_t ws_bytes, int64_t* err, dyq_stream_t stream);
+
+/* Force the kernel family (testing / benchmarking): 0 = auto (default),
+ * 1 = decode (M <= 64 only), 2 = prefill.  Process-wide. */
+DYQ_API dyq_status_t dyq_set_path(int32_t path);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYQ_H */

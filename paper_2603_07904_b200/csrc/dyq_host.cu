@@ -1,0 +1,282 @@
+// dyq_host.cu -- the C ABI of include/dyq.h: argument validation, sizing, plans
+// and kernel routing.  No allocation, no host synchronization on the hot path.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <climits>
+
+#include "dyq_internal.cuh"
+
+namespace dyq {
+
+static thread_local char g_err[512] = "";
+int g_path = 0;  // 0 auto, 1 decode, 2 prefill (read by the router)
+
+dyq_status_t set_error(dyq_status_t st, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+dyq_status_t check_launch(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return DYQ_OK;
+}
+
+bool make_layout(const dyq_wdesc_t* wd, WLayout* L) {
+    if (!wd) return false;
+    L->N = wd->N;
+    L->K = wd->K;
+    L->G = wd->group;
+    L->wbits = wd->wbits;
+    L->round_mode = wd->round_mode;
+    if (L->N <= 0 || L->K <= 0 || L->G <= 0) return false;
+    L->NG = L->K / L->G;
+    L->NSP = L->K / 64;
+    L->T128 = (L->N + 127) / 128;
+    L->nsub_last = (L->N - 128 * (L->T128 - 1)) / 16;
+    L->chunk = 512 * (L->wbits / 4);
+    L->codes_bytes = (size_t)L->N * L->K * L->wbits / 8;
+    const size_t slots = (size_t)L->T128 * L->NG * 128;
+    L->scales_bytes = slots * 4;
+    L->zeros_off = L->scales_bytes;
+    L->meta_bytes = L->scales_bytes + ((slots + 15) & ~(size_t)15);
+    return true;
+}
+
+ActLayoutDec act_layout_dec(const WLayout& L) {
+    ActLayoutDec A;
+    A.xq_off = 0;
+    A.par_off = ((size_t)DEC_MPAD * L.K + 255) & ~(size_t)255;
+    A.bytes = A.par_off + (((size_t)L.NG * DEC_MPAD * 8 + 255) & ~(size_t)255);
+    return A;
+}
+
+static dyq_status_t validate_wdesc(const dyq_wdesc_t* wd, WLayout* L) {
+    if (!wd) return set_error(DYQ_EINVAL, "null weight descriptor");
+    if (wd->wbits != 4 && wd->wbits != 8)
+        return set_error(DYQ_EINVAL, "wbits must be 4 or 8 (got %d)", wd->wbits);
+    if (wd->group != 64 && wd->group != 128)
+        return set_error(DYQ_ESHAPE, "group must be 64 or 128 (got %d)", wd->group);
+    if (wd->N <= 0 || wd->K <= 0) return set_error(DYQ_ESHAPE, "N, K must be positive");
+    if (wd->N % 16) return set_error(DYQ_ESHAPE, "N %% 16 != 0 (N=%d)", wd->N);
+    if (wd->K % wd->group) return set_error(DYQ_ESHAPE, "K %% group != 0 (K=%d, G=%d)", wd->K, wd->group);
+    if (wd->round_mode != 0 && wd->round_mode != 1) return set_error(DYQ_EINVAL, "round_mode must be 0 or 1");
+    if (!make_layout(wd, L)) return set_error(DYQ_ESHAPE, "bad layout");
+    return DYQ_OK;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+}  // namespace dyq
+
+using namespace dyq;
+
+extern "C" {
+
+const char* dyq_last_error(void) { return g_err; }
+const char* dyq_version(void) { return "dyq 0.1 sm_100a"; }
+
+dyq_status_t dyq_set_path(int32_t path) {
+    if (path < 0 || path > 2) return set_error(DYQ_EINVAL, "path must be 0, 1 or 2");
+    g_path = path;
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_error_reset(int64_t* err, dyq_stream_t stream) {
+    if (!err) return set_error(DYQ_EINVAL, "null err");
+    static const int64_t none = INT64_MAX;
+    // 8-byte pageable source: staged by the driver before return
+    if (cudaMemcpyAsync(err, &none, sizeof none, cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
+        return check_launch("dyq_error_reset");
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_error_read(const int64_t* err, int64_t* host_index, dyq_stream_t stream) {
+    if (!err || !host_index) return set_error(DYQ_EINVAL, "null pointer");
+    int64_t v = INT64_MAX;
+    if (cudaMemcpyAsync(&v, err, sizeof v, cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess ||
+        cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+        return check_launch("dyq_error_read");
+    *host_index = v;
+    if (v != INT64_MAX) return set_error(DYQ_ENONFINITE, "non-finite input at linear index %lld", (long long)v);
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_pack_weights_size(const dyq_wdesc_t* wd, size_t* codes_bytes, size_t* meta_bytes) {
+    WLayout L;
+    dyq_status_t rc = validate_wdesc(wd, &L);
+    if (rc) return rc;
+    if (!codes_bytes || !meta_bytes) return set_error(DYQ_EINVAL, "null size pointer");
+    *codes_bytes = L.codes_bytes;
+    *meta_bytes = L.meta_bytes;
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_pack_weights(const dyq_wdesc_t* wd, const uint16_t* w_bf16, void* codes, void* meta,
+                              int64_t* err, dyq_stream_t stream) {
+    WLayout L;
+    dyq_status_t rc = validate_wdesc(wd, &L);
+    if (rc) return rc;
+    if (!w_bf16 || !codes || !meta) return set_error(DYQ_EINVAL, "null pointer");
+    if (!aligned16(codes) || !aligned16(meta)) return set_error(DYQ_EINVAL, "codes/meta must be 16-byte aligned");
+    return launch_pack(L, w_bf16, codes, meta, err, (cudaStream_t)stream);
+}
+
+dyq_status_t dyq_unpack_for_check(const dyq_wdesc_t* wd, const void* codes, const void* meta, uint8_t* q,
+                                  float* s, uint8_t* z, dyq_stream_t stream) {
+    WLayout L;
+    dyq_status_t rc = validate_wdesc(wd, &L);
+    if (rc) return rc;
+    if (!codes || !meta || !q || !s || !z) return set_error(DYQ_EINVAL, "null pointer");
+    return launch_unpack(L, codes, meta, q, s, z, (cudaStream_t)stream);
+}
+
+static dyq_status_t validate_calib(const dyq_calib_t* c) {
+    if (!c) return set_error(DYQ_EINVAL, "null calibration table");
+    if (!(0.0 <= c->theta_24 && c->theta_24 <= c->theta_48 && c->theta_48 <= c->theta_fp))
+        return set_error(DYQ_EINVAL, "thresholds must satisfy 0 <= theta_24 <= theta_48 <= theta_fp (S:198)");
+    if (!(c->lambda >= 0.0 && c->lambda <= 1.0)) return set_error(DYQ_EINVAL, "lambda must be in [0,1]");
+    if (!(c->D_acc > 0.0) || !(c->eta > 0.0)) return set_error(DYQ_EINVAL, "D_acc and eta must be > 0 (S:199)");
+    if (!(c->J_cap > 0.0)) return set_error(DYQ_EINVAL, "J_cap must be > 0");
+    if (c->K < 1) return set_error(DYQ_EINVAL, "K must be >= 1 (S:199)");
+    if (c->W_macro < 1 || c->W_macro > 64 || c->W_micro < 1 || c->W_micro > 64)
+        return set_error(DYQ_EINVAL, "windows must be in [1,64]");
+    if (c->H < 1 || c->H > 1024) return set_error(DYQ_EINVAL, "H must be in [1,1024]");
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_state_size(int32_t E, const dyq_calib_t* calib, size_t* bytes) {
+    dyq_status_t rc = validate_calib(calib);
+    if (rc) return rc;
+    if (E <= 0 || E > (1 << 20)) return set_error(DYQ_ESHAPE, "E out of range");
+    if (!bytes) return set_error(DYQ_EINVAL, "null bytes");
+    *bytes = sel_state_bytes(E, *calib);
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_state_init(int32_t E, const dyq_calib_t* calib, void* state, dyq_stream_t stream) {
+    dyq_status_t rc = validate_calib(calib);
+    if (rc) return rc;
+    if (E <= 0 || E > (1 << 20)) return set_error(DYQ_ESHAPE, "E out of range");
+    if (!state || !aligned16(state)) return set_error(DYQ_EINVAL, "state must be a 16-byte aligned device buffer");
+    return launch_sel_init(E, *calib, state, (cudaStream_t)stream);
+}
+
+// E is needed for the grid; the reset kernel reads it from the device header,
+// so launch for the maximum and let threads beyond E exit.
+dyq_status_t dyq_state_reset_episode(void* state, const uint8_t* mask, dyq_stream_t stream) {
+    if (!state) return set_error(DYQ_EINVAL, "null state");
+    return launch_sel_reset(state, 1 << 16, mask, (cudaStream_t)stream);
+}
+
+dyq_status_t dyq_select_bits(void* state, int32_t E, const float* prev_action, int32_t* bits, double* S_out,
+                             int32_t* target_out, dyq_stream_t stream) {
+    if (!state || !bits) return set_error(DYQ_EINVAL, "null pointer");
+    if (E <= 0 || E > (1 << 20)) return set_error(DYQ_ESHAPE, "E out of range");
+    return launch_select(state, E, 1024, prev_action, bits, S_out, target_out, (cudaStream_t)stream);
+}
+
+dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t tpe, const int32_t* abits_of_host,
+                            int32_t* row_bits, dyq_stream_t stream) {
+    if (!bits || !row_bits) return set_error(DYQ_EINVAL, "null pointer");
+    if (E <= 0 || tpe <= 0) return set_error(DYQ_ESHAPE, "E and tokens_per_episode must be positive");
+    if (abits_of_host)
+        for (int i = 0; i < 4; ++i) {
+            const int b = abits_of_host[i];
+            if (b != 2 && b != 4 && b != 8 && b != 16) return set_error(DYQ_EINVAL, "abits_of entries must be 2/4/8/16");
+        }
+    return launch_route(bits, E, tpe, abits_of_host, row_bits, (cudaStream_t)stream);
+}
+
+dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* bytes) {
+    WLayout L;
+    dyq_status_t rc = validate_wdesc(wd, &L);
+    if (rc) return rc;
+    if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range [0, 65536]");
+    if (!bytes) return set_error(DYQ_EINVAL, "null bytes");
+    const ActLayoutDec A = act_layout_dec(L);
+    *bytes = A.bytes;
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_workspace_init(void* ws, size_t bytes, dyq_stream_t stream) {
+    if (!ws && bytes) return set_error(DYQ_EINVAL, "null workspace");
+    if (bytes && cudaMemsetAsync(ws, 0, bytes, (cudaStream_t)stream) != cudaSuccess)
+        return check_launch("dyq_workspace_init");
+    return DYQ_OK;
+}
+
+static dyq_status_t qlinear_common(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x,
+                                   int32_t M, const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype,
+                                   int32_t* I, void* ws, size_t ws_bytes, int64_t* err, cudaStream_t st) {
+    WLayout L;
+    dyq_status_t rc = validate_wdesc(wd, &L);
+    if (rc) return rc;
+    if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range [0, 65536]");
+    if (M == 0) return DYQ_OK;
+    if (!codes || !meta || !x || !ws || (!y && !I)) return set_error(DYQ_EINVAL, "null pointer");
+    if (!aligned16(codes) || !aligned16(meta) || !aligned16(ws) || !aligned16(x))
+        return set_error(DYQ_EINVAL, "codes/meta/x/workspace must be 16-byte aligned");
+    if (!row_bits && bits != 2 && bits != 4 && bits != 8 && bits != 16)
+        return set_error(DYQ_EINVAL, "bits must be 2, 4, 8 or 16 (got %d)", bits);
+    if (y && y_dtype != 0 && y_dtype != 1) return set_error(DYQ_EINVAL, "y_dtype must be 0 (fp32) or 1 (bf16)");
+    size_t need = 0;
+    dyq_qlinear_workspace(wd, M, &need);
+    if (ws_bytes < need) return set_error(DYQ_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, need);
+    // Decode path: 16-token tiles (the prefill kernel takes large M when built).
+    for (int m0 = 0; m0 < M; m0 += DEC_MPAD) {
+        const int mt = (M - m0) < DEC_MPAD ? (M - m0) : DEC_MPAD;
+        rc = launch_actquant_dec(L, x, mt, m0, row_bits, bits, ws, err, st);
+        if (rc) return rc;
+        rc = launch_decode(L, codes, meta, x, mt, m0, M, row_bits, bits, y, y_dtype, I, ws, st);
+        if (rc) return rc;
+    }
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_qlinear(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x, int32_t M,
+                         const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype, void* workspace,
+                         size_t ws_bytes, int64_t* err, dyq_stream_t stream) {
+    if (!y && M > 0) return set_error(DYQ_EINVAL, "null y");
+    return qlinear_common(wd, codes, meta, x, M, row_bits, bits, y, y_dtype, nullptr, workspace, ws_bytes, err,
+                          (cudaStream_t)stream);
+}
+
+dyq_status_t dyq_qlinear_i32_partials(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x,
+                                      int32_t M, const int32_t* row_bits, int32_t bits, int32_t* I, void* workspace,
+                                      size_t ws_bytes, int64_t* err, dyq_stream_t stream) {
+    if (!I && M > 0) return set_error(DYQ_EINVAL, "null I");
+    return qlinear_common(wd, codes, meta, x, M, row_bits, bits, nullptr, 0, I, workspace, ws_bytes, err,
+                          (cudaStream_t)stream);
+}
+
+dyq_status_t dyq_act_quant_for_check(const dyq_wdesc_t* wd, const uint16_t* x, int32_t M, const int32_t* row_bits,
+                                     int32_t bits, uint8_t* xq, float* sx, uint8_t* zx, int32_t* SX, void* ws,
+                                     size_t ws_bytes, int64_t* err, dyq_stream_t stream) {
+    WLayout L;
+    dyq_status_t rc = validate_wdesc(wd, &L);
+    if (rc) return rc;
+    if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range");
+    if (!x || !xq || !sx || !zx || !SX || !ws) return set_error(DYQ_EINVAL, "null pointer");
+    if (!row_bits && bits != 2 && bits != 4 && bits != 8 && bits != 16)
+        return set_error(DYQ_EINVAL, "bits must be 2, 4, 8 or 16");
+    size_t need = 0;
+    dyq_qlinear_workspace(wd, M, &need);
+    if (ws_bytes < need) return set_error(DYQ_EINVAL, "workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int m0 = 0; m0 < M; m0 += DEC_MPAD) {
+        const int mt = (M - m0) < DEC_MPAD ? (M - m0) : DEC_MPAD;
+        rc = launch_actquant_dec(L, x, mt, m0, row_bits, bits, ws, err, st);
+        if (rc) return rc;
+        rc = launch_actquant_export(L, mt, ws, xq, sx, zx, SX, m0, st);
+        if (rc) return rc;
+    }
+    return DYQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+// dyq_internal.cuh -- layouts, launch-plan structs and small device helpers
+// shared by the libdyq.so translation units.  Product code: never includes
+// anything under oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/dyq.h"
+
+namespace dyq {
+
+// ------------------------------------------------------------------ layout
+// Packed weights (DESIGN.md §"Data layout in HBM").
+//   rows are grouped in 128-row tiles; a tile holds up to 8 sub-tiles of 16
+//   rows (the last tile may be ragged: N % 16 == 0 is required);
+//   K is walked in "slab pairs" of 64 input channels (two 32-wide MMA k-steps).
+//   One chunk = (tile, slab pair, sub-tile) = 16 rows x 64 k:
+//     W4: 512 B = 32 lanes x 16 B, lane L = 4*gid + t (gid = row % 8, t = 0..3)
+//         holds [slab0 word(row gid)][slab0 word(row gid+8)]
+//               [slab1 word(row gid)][slab1 word(row gid+8)],
+//         word byte b: lo nibble = q[k = 32*slab + 4t + b],
+//                      hi nibble = q[k = 32*slab + 16 + 4t + b].
+//     W8: 1024 B = [slab (2)][lane (32)][16 B = R0 R1 R2 R3], the u8 A-fragment
+//         registers of mma.m16n8k32: R0 = q[gid][4t..4t+3], R1 = q[gid+8][4t..],
+//         R2 = q[gid][16+4t..], R3 = q[gid+8][16+4t..] (k relative to the slab).
+//   Chunks are ordered (tile, slab pair, sub-tile) so that one (tile, slab pair)
+//   is 8 contiguous chunks (4 KB for W4) -- one bulk copy for the prefill kernel.
+// Metadata: scales fp32 then zero-points u8, each indexed
+//   ((tile * NG + g) * 8 + sub) * 16 + p,  p = 2 * (r % 8) + r / 8,
+//   r = row within the sub-tile: the decode lane of group gid reads the
+//   (row gid, row gid+8) pair with one 8-byte (scales) / 2-byte (zeros) load.
+
+struct WLayout {
+    int N, K, G, wbits, round_mode;
+    int NG;       // K / G
+    int NSP;      // K / 64 slab pairs
+    int T128;     // ceil(N / 128)
+    int nsub_last;
+    int chunk;    // bytes per (tile, sp, sub) chunk
+    size_t codes_bytes, scales_bytes, zeros_off, meta_bytes;
+};
+
+__host__ __device__ inline size_t chunk_offset(const WLayout& L, int tile, int sp, int sub) {
+    const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
+    return ((size_t)tile * L.NSP * 8 + (size_t)sp * nsub + sub) * (size_t)L.chunk;
+}
+__host__ __device__ inline size_t meta_index(const WLayout& L, int tile, int g, int sub, int r) {
+    return (((size_t)tile * L.NG + g) * 8 + sub) * 16 + 2 * (r & 7) + (r >> 3);
+}
+
+// Activation codes for the decode kernel: [Mpad = 16][K] u8, each 64-k group
+// permuted so that decode lane t reads its 4 B-fragment words with one 16-byte
+// load: position t*16 + s*8 + h*4 + b  <->  k = 32*s + 16*h + 4*t + b.
+// Per (group g, token m) parameters {float s_x; uint32 (z_x << 16) | SX}
+// at [g][Mpad][8 B] so that the lane owning tokens (2t, 2t+1) reads 16 B.
+constexpr int DEC_MPAD = 16;
+__host__ __device__ inline int dec_perm(int kk) {  // kk in [0,64) -> position
+    const int s = kk >> 5, h = (kk >> 4) & 1, t = (kk >> 2) & 3, b = kk & 3;
+    return t * 16 + s * 8 + h * 4 + b;
+}
+
+struct ActLayoutDec {
+    size_t xq_off, par_off, bytes;
+};
+
+// ------------------------------------------------------------ error words
+__device__ inline void report_nonfinite(int64_t* err, int64_t idx) {
+    if (err) atomicMin(reinterpret_cast<unsigned long long*>(err), (unsigned long long)idx);
+}
+
+__device__ inline float bf16_bits_to_float(uint16_t h) {
+    return __uint_as_float(((uint32_t)h) << 16);
+}
+
+// ------------------------------------------------- exact quantizer pieces
+// Fit of DESIGN.md readings 2-4 (restated from PAPER.md Eq. 2, P:100-106 and
+// SPEC S:43-51): lo = min(0, min v), hi = max(0, max v) (exact), R = max(hi-lo,
+// 1e-8) in fp64, s64 = R / (2^b-1), stored s = fp32(s64), z = clamp(half-up(-lo/s64)).
+// Explicit _rn intrinsics: no contraction, IEEE rounding.
+__device__ inline void fit_params(float vmin, float vmax, int bits, float* s_out, int* z_out) {
+    double lo = vmin < 0.f ? (double)vmin : 0.0;
+    double hi = vmax > 0.f ? (double)vmax : 0.0;
+    const double levels = (double)((1 << bits) - 1);
+    double R = __dadd_rn(hi, -lo);
+    if (R < 1e-8) R = 1e-8;
+    const double s64 = __ddiv_rn(R, levels);
+    const double zr = __ddiv_rn(-lo, s64);
+    const double fl = floor(zr);
+    double zq = fl + ((__dadd_rn(zr, -fl) >= 0.5) ? 1.0 : 0.0);
+    if (zq < 0.0) zq = 0.0;
+    if (zq > levels) zq = levels;
+    *s_out = __double2float_rn(s64);
+    *z_out = (int)zq;
+}
+
+// Eq. (2): q = clamp(floor(v / s) + z, 0, 2^b - 1), floor of the fp64 quotient of
+// the fp32 operands (exact for the in-range quotients, reading 4).
+__device__ inline int quantize_one(float v, float s, int z, int bits, int round_mode) {
+    const double r = __ddiv_rn((double)v, (double)s);
+    double f = round_mode == 1 ? floor(__dadd_rn(r, 0.5)) : floor(r);
+    double c = f + (double)z;
+    const double levels = (double)((1 << bits) - 1);
+    c = c < 0.0 ? 0.0 : (c > levels ? levels : c);
+    return (int)c;
+}
+
+__device__ inline bool finite_f(float v) { return isfinite(v); }
+
+// -------------------------------------------------------------- warp ops
+__device__ inline float warp_min(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ inline float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ inline int warp_sum_i(int v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// dyq_select.cu
+size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
+dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);
+dyq_status_t launch_sel_reset(void* state, int32_t E, const uint8_t* mask, cudaStream_t st);
+dyq_status_t launch_select(void* state, int32_t E, int32_t H, const float* prev_action, int32_t* bits,
+                           double* S_out, int32_t* target_out, cudaStream_t st);
+dyq_status_t launch_route(const int32_t* bits, int32_t E, int32_t tpe, const int32_t* tab4, int32_t* row_bits,
+                          cudaStream_t st);
+}  // namespace dyq
+
+// host-side helpers (dyq_host.cu)
+namespace dyq {
+dyq_status_t set_error(dyq_status_t st, const char* fmt, ...);
+dyq_status_t check_launch(const char* what);
+bool make_layout(const dyq_wdesc_t* wd, WLayout* L);
+ActLayoutDec act_layout_dec(const WLayout& L);
+
+// kernel launchers (one per TU)
+dyq_status_t launch_pack(const WLayout& L, const uint16_t* w, void* codes, void* meta,
+                         int64_t* err, cudaStream_t st);
+dyq_status_t launch_unpack(const WLayout& L, const void* codes, const void* meta, uint8_t* q,
+                           float* s, uint8_t* z, cudaStream_t st);
+dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int m0, const int32_t* row_bits,
+                                 int bits, void* ws, int64_t* err, cudaStream_t st);
+dyq_status_t launch_actquant_export(const WLayout& L, int M, const void* ws, uint8_t* xq, float* sx,
+                                    uint8_t* zx, int32_t* SX, int m0, cudaStream_t st);
+// rows m0 .. m0+M-1 (M <= DEC_MPAD); x, row_bits, y, I_out are base pointers
+dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x,
+                           int M, int m0, int Mtotal, const int32_t* row_bits, int bits, void* y,
+                           int y_dtype, int32_t* I_out, const void* ws, cudaStream_t st);
+// dyq_select.cu
+size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
+dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);
+dyq_status_t launch_sel_reset(void* state, int32_t E, const uint8_t* mask, cudaStream_t st);
+dyq_status_t launch_select(void* state, int32_t E, int32_t H, const float* prev_action, int32_t* bits,
+                           double* S_out, int32_t* target_out, cudaStream_t st);
+dyq_status_t launch_route(const int32_t* bits, int32_t E, int32_t tpe, const int32_t* tab4, int32_t* row_bits,
+                          cudaStream_t st);
+}  // namespace dyq

@@ -1,0 +1,256 @@
+// dyq_select.cu -- kinematic proxies -> S_t -> bhat_t -> Alg. 1 (b*_t), on device.
+//
+// PAPER.md: Motion Fineness M_t = 1 - ||a^xyz||/mu_max and Angular Jerk
+// J_t = ||a^rot_t - a^rot_{t-1}||/nu_max with 95th-percentile normalizers
+// (P:175-177); window means over W_macro / W_micro; fused
+// S_t = max(0, lambda*M~ + (1-lambda)*J~); bhat_t = 16 if S_t > theta_fp
+// else Phi(S_t) (Alg. 1 line 2; Eq. 6); the saturating
+// counter dispatcher (Alg. 1 lines 3-9).  The paper runs this on the
+// CPU and writes b* into zero-copy memory; here it is one tiny
+// in-stream kernel that writes bits[] in device memory, so the qlinear kernels
+// route on it without a host round trip (DESIGN.md conflict C3).
+//
+// Bit-exactness with the oracle: fp64 everywhere, explicit _rn intrinsics (no
+// FMA contraction), the oracle's evaluation order, nearest-rank percentile by
+// parallel rank counting (the k-th smallest value is unique even with ties).
+#include "dyq_internal.cuh"
+
+namespace dyq {
+
+struct SelHeader {
+    dyq_calib_t cal;
+    int32_t E;
+    int32_t stride;  // bytes per stream
+    int32_t off_jerk, off_Mwin, off_Jwin, off_prev, off_int;
+};
+constexpr size_t SEL_HDR = 256;
+static_assert(sizeof(SelHeader) <= SEL_HDR, "header");
+
+enum { I_HIST_N = 0, I_HIST_POS, I_MW_N, I_MW_POS, I_JW_N, I_JW_POS, I_STEPS, I_BSTAR, I_C, I_BBAR, I_COUNT };
+
+__host__ inline SelHeader make_sel_header(int32_t E, const dyq_calib_t& c) {
+    SelHeader h{};
+    h.cal = c;
+    h.E = E;
+    int off = c.H * 8;  // mag
+    h.off_jerk = off;
+    off += c.H * 8;
+    h.off_Mwin = off;
+    off += c.W_macro * 8;
+    h.off_Jwin = off;
+    off += c.W_micro * 8;
+    h.off_prev = off;
+    off += 3 * 8;
+    h.off_int = off;
+    off += I_COUNT * 4;
+    h.stride = (off + 15) & ~15;
+    return h;
+}
+
+size_t sel_state_bytes(int32_t E, const dyq_calib_t& c) {
+    return SEL_HDR + (size_t)E * make_sel_header(E, c).stride;
+}
+
+__device__ inline void reset_episode_dev(const SelHeader& h, uint8_t* base) {
+    int32_t* I = reinterpret_cast<int32_t*>(base + h.off_int);
+    double* prev = reinterpret_cast<double*>(base + h.off_prev);
+    I[I_MW_N] = I[I_MW_POS] = I[I_JW_N] = I[I_JW_POS] = 0;
+    I[I_STEPS] = 0;
+    I[I_BSTAR] = 16; I[I_C] = 0; I[I_BBAR] = 16;
+    prev[0] = prev[1] = prev[2] = 0.0;
+}
+
+__global__ void sel_init_kernel(uint8_t* state) {
+    const SelHeader h = *reinterpret_cast<const SelHeader*>(state);
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= h.E) return;
+    uint8_t* base = state + SEL_HDR + (size_t)e * h.stride;
+    int32_t* I = reinterpret_cast<int32_t*>(base + h.off_int);
+    I[I_HIST_N] = I[I_HIST_POS] = 0;
+    reset_episode_dev(h, base);
+}
+
+__global__ void sel_reset_kernel(uint8_t* state, const uint8_t* mask) {
+    const SelHeader h = *reinterpret_cast<const SelHeader*>(state);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < h.E; e += gridDim.x * blockDim.x) {
+        if (mask && !mask[e]) continue;
+        reset_episode_dev(h, state + SEL_HDR + (size_t)e * h.stride);
+    }
+}
+
+// k-th smallest (1-based) of v[0..n) by rank counting; all threads participate.
+__device__ double kth_smallest(const double* v, int n, int k, double* result_slot) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double x = v[i];
+        int less = 0, leq = 0;
+        for (int j = 0; j < n; ++j) {
+            const double y = v[j];
+            less += (y < x);
+            leq += (y <= x);
+        }
+        if (less < k && k <= leq) *result_slot = x;  // equal values write the same bits
+    }
+    __syncthreads();
+    return *result_slot;
+}
+
+__device__ inline double window_mean(const double* w, int cap, int n, int pos) {
+    if (n == 0) return 0.0;
+    const int start = (pos - n + cap) % cap;
+    double sum = 0.0;
+    for (int i = 0; i < n; ++i) sum = __dadd_rn(sum, w[(start + i) % cap]);
+    return __ddiv_rn(sum, (double)n);
+}
+
+__device__ inline int phi_dev(double S, double t24, double t48) {
+    if (S <= t24) return 2;
+    if (S <= t48) return 4;
+    return 8;
+}
+
+__global__ void select_bits_kernel(uint8_t* state, const float* __restrict__ prev_action, int32_t* bits,
+                                   double* S_out, int32_t* target_out) {
+    extern __shared__ double sh[];  // mag[H], jerk[H], 2 result slots
+    const SelHeader h = *reinterpret_cast<const SelHeader*>(state);
+    const dyq_calib_t& c = h.cal;
+    const int e = blockIdx.x;
+    uint8_t* base = state + SEL_HDR + (size_t)e * h.stride;
+    double* mag = reinterpret_cast<double*>(base);
+    double* jerk = reinterpret_cast<double*>(base + h.off_jerk);
+    double* Mwin = reinterpret_cast<double*>(base + h.off_Mwin);
+    double* Jwin = reinterpret_cast<double*>(base + h.off_Jwin);
+    double* prev = reinterpret_cast<double*>(base + h.off_prev);
+    int32_t* I = reinterpret_cast<int32_t*>(base + h.off_int);
+    double* smag = sh;
+    double* sjerk = sh + c.H;
+    double* slot = sh + 2 * c.H;
+    __shared__ double s_magv, s_jerkv;
+    __shared__ int s_n;
+    const bool observe = prev_action != nullptr;
+
+    if (observe) {
+        if (threadIdx.x == 0) {
+            const float* a = prev_action + (size_t)e * 7;
+            const double x = a[0], y = a[1], z = a[2];
+            const double r0 = a[3], r1 = a[4], r2 = a[5];
+            // ||a^xyz||_2 left to right, no contraction
+            const double mv = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+            double jv = 0.0;  // first observation: J = 0 (reading 16)
+            if (I[I_STEPS] > 0) {
+                const double d0 = __dadd_rn(r0, -prev[0]);
+                const double d1 = __dadd_rn(r1, -prev[1]);
+                const double d2 = __dadd_rn(r2, -prev[2]);
+                jv = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)));
+            }
+            prev[0] = r0; prev[1] = r1; prev[2] = r2;
+            const int pos = I[I_HIST_POS];
+            mag[pos] = mv;
+            jerk[pos] = jv;
+            I[I_HIST_POS] = (pos + 1) % c.H;
+            if (I[I_HIST_N] < c.H) I[I_HIST_N] += 1;
+            s_magv = mv;
+            s_jerkv = jv;
+            s_n = I[I_HIST_N];
+        }
+        __syncthreads();
+        const int n = s_n;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            smag[i] = mag[i];
+            sjerk[i] = jerk[i];
+        }
+        __syncthreads();
+        const int k = (95 * n + 99) / 100;  // nearest rank, ceil(0.95 n)
+        double mu = kth_smallest(smag, n, k, &slot[0]);
+        double nu = kth_smallest(sjerk, n, k, &slot[1]);
+        if (threadIdx.x == 0) {
+            if (mu < 1e-6) mu = 1e-6;
+            if (nu < 1e-6) nu = 1e-6;
+            double M = __dadd_rn(1.0, -__ddiv_rn(s_magv, mu));
+            if (c.clamp_M) {
+                if (M < 0.0) M = 0.0;
+                if (M > 1.0) M = 1.0;
+            }
+            double J = __ddiv_rn(s_jerkv, nu);
+            if (J > c.J_cap) J = c.J_cap;
+            int p = I[I_MW_POS];
+            Mwin[p] = M;
+            I[I_MW_POS] = (p + 1) % c.W_macro;
+            if (I[I_MW_N] < c.W_macro) I[I_MW_N] += 1;
+            p = I[I_JW_POS];
+            Jwin[p] = J;
+            I[I_JW_POS] = (p + 1) % c.W_micro;
+            if (I[I_JW_N] < c.W_micro) I[I_JW_N] += 1;
+            I[I_STEPS] += 1;
+        }
+    }
+    if (threadIdx.x != 0) return;
+    const double Mbar = window_mean(Mwin, c.W_macro, I[I_MW_N], I[I_MW_POS]);
+    const double Jbar = window_mean(Jwin, c.W_micro, I[I_JW_N], I[I_JW_POS]);
+    const double lam_term = __dmul_rn(c.lambda, Mbar);
+    const double one_minus = __dadd_rn(1.0, -c.lambda);
+    const double jer_term = __dmul_rn(one_minus, Jbar);
+    double S = __dadd_rn(lam_term, jer_term);
+    if (S < 0.0) S = 0.0;
+    const bool warm = I[I_STEPS] < c.W_macro;
+    int bhat;
+    if (warm || S > c.theta_fp) bhat = 16;
+    else bhat = phi_dev(S, c.theta_24, c.theta_48);
+    // Alg. 1 lines 3-9
+    int bstar = I[I_BSTAR], cnt = I[I_C], bbar = I[I_BBAR];
+    if (bhat >= bstar) {
+        bstar = bhat; cnt = 0; bbar = bhat;
+    } else {
+        const int carried = cnt > 0 ? bbar : 0;
+        const int nb = bhat > carried ? bhat : carried;
+        const int nc = cnt * (nb == bbar ? 1 : 0) + 1;
+        bstar = nc == c.K ? nb : bstar;
+        cnt = nc % c.K;
+        bbar = nb;
+    }
+    I[I_BSTAR] = bstar; I[I_C] = cnt; I[I_BBAR] = bbar;
+    bits[e] = bstar;
+    if (S_out) S_out[e] = S;
+    if (target_out) target_out[e] = bhat;
+}
+
+__global__ void route_bits_kernel(const int32_t* bits, int E, int tpe, int4 tab, int32_t* row_bits) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= E * tpe) return;
+    const int b = bits[m / tpe];
+    row_bits[m] = b == 2 ? tab.x : b == 4 ? tab.y : b == 8 ? tab.z : tab.w;
+}
+
+dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st) {
+    const SelHeader h = make_sel_header(E, c);
+    cudaMemsetAsync(state, 0, sel_state_bytes(E, c), st);
+    cudaMemcpyAsync(state, &h, sizeof h, cudaMemcpyHostToDevice, st);  // pageable: staged synchronously
+    sel_init_kernel<<<(E + 127) / 128, 128, 0, st>>>(reinterpret_cast<uint8_t*>(state));
+    return check_launch("sel_init_kernel");
+}
+
+dyq_status_t launch_sel_reset(void* state, int32_t E, const uint8_t* mask, cudaStream_t st) {
+    (void)E;  // E lives in the device header; the kernel strides over it
+    sel_reset_kernel<<<8, 256, 0, st>>>(reinterpret_cast<uint8_t*>(state), mask);
+    return check_launch("sel_reset_kernel");
+}
+
+dyq_status_t launch_select(void* state, int32_t E, int32_t H, const float* prev_action, int32_t* bits,
+                           double* S_out, int32_t* target_out, cudaStream_t st) {
+    // H is only known on the device (state header); size for the maximum
+    const int threads = 256;
+    (void)H;
+    const size_t smem = (size_t)(2 * 1024 + 2) * sizeof(double);
+    select_bits_kernel<<<E, threads, smem, st>>>(reinterpret_cast<uint8_t*>(state), prev_action, bits, S_out,
+                                                  target_out);
+    return check_launch("select_bits_kernel");
+}
+
+dyq_status_t launch_route(const int32_t* bits, int32_t E, int32_t tpe, const int32_t* tab4, int32_t* row_bits,
+                          cudaStream_t st) {
+    const int4 tab = tab4 ? make_int4(tab4[0], tab4[1], tab4[2], tab4[3]) : make_int4(2, 4, 8, 16);
+    const int total = E * tpe;
+    route_bits_kernel<<<(total + 255) / 256, 256, 0, st>>>(bits, E, tpe, tab, row_bits);
+    return check_launch("route_bits_kernel");
+}
+
+}  // namespace dyq

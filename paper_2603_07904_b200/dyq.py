@@ -1,0 +1,244 @@
+"""Thin Python binding of include/dyq.h (libdyq.so) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libdyq.so; this module
+only converts torch tensors to raw device pointers / streams and raises on a
+non-OK status.  PyTorch provides device memory and streams (plumbing).  There is
+no CPU fallback: if libdyq.so is missing or no CUDA device is present the calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdyq.so")
+
+P, i32, i64, f64, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_size_t
+
+# name -> argtypes (restype dyq_status_t unless listed in _RESTYPES)
+_SIGS = {
+    "dyq_last_error": [],
+    "dyq_version": [],
+    "dyq_error_reset": [P, P],
+    "dyq_error_read": [P, P, P],
+    "dyq_pack_weights_size": [P, P, P],
+    "dyq_pack_weights": [P, P, P, P, P, P],
+    "dyq_unpack_for_check": [P, P, P, P, P, P, P],
+    "dyq_state_size": [i32, P, P],
+    "dyq_state_init": [i32, P, P, P],
+    "dyq_state_reset_episode": [P, P, P],
+    "dyq_select_bits": [P, i32, P, P, P, P, P],
+    "dyq_route_bits": [P, i32, i32, P, P, P],
+    "dyq_qlinear_workspace": [P, i32, P],
+    "dyq_workspace_init": [P, sz, P],
+    "dyq_qlinear": [P, P, P, P, i32, P, i32, P, i32, P, sz, P, P],
+    "dyq_qlinear_i32_partials": [P, P, P, P, i32, P, i32, P, P, sz, P, P],
+    "dyq_act_quant_for_check": [P, P, i32, P, i32, P, P, P, P, P, sz, P, P],
+    "dyq_set_path": [i32],
+}
+_RESTYPES = {"dyq_last_error": C.c_char_p, "dyq_version": C.c_char_p}
+
+STATUS = {0: "DYQ_OK", 1: "DYQ_EINVAL", 2: "DYQ_ESHAPE", 3: "DYQ_EUNSUPPORTED",
+          4: "DYQ_ENONFINITE", 5: "DYQ_ECUDA", 6: "DYQ_ENCCL"}
+
+
+class DyqError(RuntimeError):
+    def __init__(self, code: int, fn: str, msg: str):
+        super().__init__(f"{fn} -> {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libdyq.so (build it first with paper_2603_07904_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libdyq.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = _RESTYPES.get(name, C.c_int)
+        _lib = L
+    return _lib
+
+
+def _call(name, *args):
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        raise DyqError(rc, name, lib().dyq_last_error().decode())
+    return rc
+
+
+class WDesc(C.Structure):
+    _fields_ = [("N", i32), ("K", i32), ("group", i32), ("wbits", i32), ("round_mode", i32)]
+
+
+class Calib(C.Structure):
+    """dyq_calib_t; keys per SPEC S:261."""
+    _fields_ = [("theta_24", f64), ("theta_48", f64), ("theta_fp", f64), ("lambda_", f64),
+                ("D_acc", f64), ("eta", f64), ("J_cap", f64),
+                ("K", i32), ("W_macro", i32), ("W_micro", i32), ("H", i32), ("clamp_M", i32)]
+
+
+def default_calib(**kw) -> Calib:
+    """theta_fp = 0.5, W_macro = 10, W_micro = 5; lambda = 0.5,
+    K = 3, H = 256, J_cap = 2 (SPEC defaults); Theta = (0.1, 0.3)."""
+    d = dict(theta_24=0.1, theta_48=0.3, theta_fp=0.5, lambda_=0.5, D_acc=1.0, eta=0.01,
+             J_cap=2.0, K=3, W_macro=10, W_micro=5, H=256, clamp_M=1)
+    d.update(kw)
+    return Calib(**d)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def version() -> str:
+    return lib().dyq_version().decode()
+
+
+def set_path(path: int):
+    _call("dyq_set_path", path)
+
+
+# ----------------------------------------------------------------- errors
+def error_reset(err, stream=None):
+    _call("dyq_error_reset", _ptr(err), _stream(stream))
+
+
+def error_read(err, stream=None) -> int:
+    """Returns the first non-finite element index or -1."""
+    out = C.c_int64(0)
+    rc = lib().dyq_error_read(_ptr(err), C.byref(out), _stream(stream))
+    if rc == 4:
+        return int(out.value)
+    if rc != 0:
+        raise DyqError(rc, "dyq_error_read", lib().dyq_last_error().decode())
+    return -1
+
+
+# ------------------------------------------------------------------- pack
+def pack_weights_size(wd: WDesc) -> tuple[int, int]:
+    cb, mb = C.c_size_t(0), C.c_size_t(0)
+    _call("dyq_pack_weights_size", C.byref(wd), C.byref(cb), C.byref(mb))
+    return cb.value, mb.value
+
+
+def pack_weights(wd: WDesc, w_bf16, codes, meta, err=None, stream=None):
+    _call("dyq_pack_weights", C.byref(wd), _ptr(w_bf16), _ptr(codes), _ptr(meta), _ptr(err),
+          _stream(stream))
+
+
+def unpack_for_check(wd: WDesc, codes, meta, q, s, z, stream=None):
+    _call("dyq_unpack_for_check", C.byref(wd), _ptr(codes), _ptr(meta), _ptr(q), _ptr(s), _ptr(z),
+          _stream(stream))
+
+
+# ---------------------------------------------------------- bit selection
+def state_size(E: int, calib: Calib) -> int:
+    b = C.c_size_t(0)
+    _call("dyq_state_size", E, C.byref(calib), C.byref(b))
+    return b.value
+
+
+def state_init(E: int, calib: Calib, state, stream=None):
+    _call("dyq_state_init", E, C.byref(calib), _ptr(state), _stream(stream))
+
+
+def state_reset_episode(state, mask=None, stream=None):
+    _call("dyq_state_reset_episode", _ptr(state), _ptr(mask), _stream(stream))
+
+
+def select_bits(state, E: int, prev_action, bits, S_out=None, target_out=None, stream=None):
+    _call("dyq_select_bits", _ptr(state), E, _ptr(prev_action), _ptr(bits), _ptr(S_out),
+          _ptr(target_out), _stream(stream))
+
+
+def route_bits(bits, E: int, tokens_per_episode: int, row_bits, abits_of=None, stream=None):
+    tab = None if abits_of is None else (C.c_int32 * 4)(*abits_of)
+    _call("dyq_route_bits", _ptr(bits), E, tokens_per_episode, tab, _ptr(row_bits), _stream(stream))
+
+
+# ---------------------------------------------------------------- qlinear
+def qlinear_workspace(wd: WDesc, M: int) -> int:
+    b = C.c_size_t(0)
+    _call("dyq_qlinear_workspace", C.byref(wd), M, C.byref(b))
+    return b.value
+
+
+def workspace_init(ws, stream=None):
+    _call("dyq_workspace_init", _ptr(ws), ws.numel() * ws.element_size(), _stream(stream))
+
+
+def qlinear(wd: WDesc, codes, meta, x, M: int, row_bits, bits: int, y, y_dtype: int, ws,
+            err=None, stream=None):
+    _call("dyq_qlinear", C.byref(wd), _ptr(codes), _ptr(meta), _ptr(x), M, _ptr(row_bits), bits,
+          _ptr(y), y_dtype, _ptr(ws), ws.numel() * ws.element_size(), _ptr(err), _stream(stream))
+
+
+def qlinear_i32_partials(wd: WDesc, codes, meta, x, M: int, row_bits, bits: int, I, ws,
+                         err=None, stream=None):
+    _call("dyq_qlinear_i32_partials", C.byref(wd), _ptr(codes), _ptr(meta), _ptr(x), M,
+          _ptr(row_bits), bits, _ptr(I), _ptr(ws), ws.numel() * ws.element_size(), _ptr(err),
+          _stream(stream))
+
+
+def act_quant_for_check(wd: WDesc, x, M: int, row_bits, bits: int, xq, sx, zx, SX, ws,
+                        err=None, stream=None):
+    _call("dyq_act_quant_for_check", C.byref(wd), _ptr(x), M, _ptr(row_bits), bits, _ptr(xq),
+          _ptr(sx), _ptr(zx), _ptr(SX), _ptr(ws), ws.numel() * ws.element_size(), _ptr(err),
+          _stream(stream))
+
+
+# ------------------------------------------------ torch-owned conveniences
+@dataclass
+class PackedLinear:
+    """Packed weights of one linear layer (device buffers owned by torch)."""
+    wd: WDesc
+    codes: object
+    meta: object
+
+    @classmethod
+    def from_bf16(cls, w_bf16, group: int = 64, wbits: int = 4, round_mode: int = 0, err=None,
+                  stream=None):
+        import torch
+        N, K = w_bf16.shape
+        wd = WDesc(N, K, group, wbits, round_mode)
+        cb, mb = pack_weights_size(wd)
+        dev = w_bf16.device
+        codes = torch.empty(cb, dtype=torch.uint8, device=dev)
+        meta = torch.empty(mb, dtype=torch.uint8, device=dev)
+        pack_weights(wd, w_bf16, codes, meta, err, stream)
+        return cls(wd, codes, meta)
+
+    def workspace(self, M: int):
+        import torch
+        ws = torch.zeros(max(16, qlinear_workspace(self.wd, M)), dtype=torch.uint8,
+                         device=self.codes.device)
+        return ws
+
+    def __call__(self, x, row_bits=None, bits: int = 4, out_dtype=None, ws=None, err=None,
+                 stream=None):
+        import torch
+        M = x.shape[0]
+        out_dtype = out_dtype or torch.float32
+        y = torch.empty(M, self.wd.N, dtype=out_dtype, device=x.device)
+        if ws is None:
+            ws = self.workspace(M)
+        qlinear(self.wd, self.codes, self.meta, x, M, row_bits, bits, y,
+                0 if out_dtype == torch.float32 else 1, ws, err, stream)
+        return y
