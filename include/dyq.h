@@ -178,6 +178,23 @@ DYQ_API dyq_status_t dyq_qlinear(const dyq_wdesc_t* wd, const void* codes, const
                          int32_t bits, void* y, int32_t y_dtype, void* workspace,
                          size_t ws_bytes, int64_t* err, dyq_stream_t stream);
 
+/* Split form of dyq_qlinear for callers that reuse one quantized activation
+ * for several linears with the same K (e.g. Q/K/V, gate/up: P:334 quantizes
+ * once per activation, not per GEMM):
+ *   dyq_act_quant  quantizes x [M,K] at row_bits into `workspace` (Eq. 2 per
+ *                  (token, group)); the workspace then holds the codes, s_x,
+ *                  z_x and SX of this activation;
+ *   dyq_qlinear_q  runs the linear layer on those codes (x is still read for
+ *                  A16 rows).  Same arguments / semantics as dyq_qlinear.
+ * Currently M <= 16 (the decode regime); larger M returns DYQ_EUNSUPPORTED. */
+DYQ_API dyq_status_t dyq_act_quant(const dyq_wdesc_t* wd, const uint16_t* x, int32_t M,
+                                   const int32_t* row_bits, int32_t bits, void* workspace,
+                                   size_t ws_bytes, int64_t* err, dyq_stream_t stream);
+DYQ_API dyq_status_t dyq_qlinear_q(const dyq_wdesc_t* wd, const void* codes, const void* meta,
+                                   const uint16_t* x, int32_t M, const int32_t* row_bits,
+                                   int32_t bits, void* y, int32_t y_dtype, void* workspace,
+                                   size_t ws_bytes, dyq_stream_t stream);
+
 /* Test hook: same main loop, writes the exact integer group sums
  * I[m,n,g] (int32 [M,N,K/G]; 0 for A16 rows) instead of y. */
 DYQ_API dyq_status_t dyq_qlinear_i32_partials(const dyq_wdesc_t* wd, const void* codes,

@@ -1,56 +1,67 @@
 // dyq_actquant.cu -- dynamic activation quantization (PAPER.md P:220, P:223:
 // the step-wise activation switches between BF16 and X in {2,4,8}; Eq. (2) per
-// (token, group), reading 6).  Decode layout (see dyq_internal.cuh).
+// (token, group), reading 6).  Writes the decode layout described in
+// dyq_internal.cuh (par / xq / x16 arrays, contiguous across K-groups).
 #include "dyq_internal.cuh"
+#include "dyq_ptx.cuh"
 
 namespace dyq {
 
-// One warp per (token m, group g); M <= DEC_MPAD tokens starting at row m0.
-// Rows of the padded tile beyond M and A16 rows get zero codes / params.
+// One warp per (group g, token m); M <= DEC_MPAD tokens starting at row m0.
+// A16 rows: zero codes / params and a bf16 copy of x in x16; padding rows
+// (m >= M): all zero.
 __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, int M, int m0,
-                                    const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ xq,
-                                    uint2* __restrict__ par, int64_t* err) {
+                                    const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ ws,
+                                    ActLayoutDec A, int64_t* err) {
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();  // x may be produced by the preceding kernel
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= DEC_MPAD * L.NG) return;
-    const int m = warp / L.NG, g = warp % L.NG;
-    uint8_t* dst = xq + (size_t)m * L.K + (size_t)g * L.G;
-    uint2* pdst = par + (size_t)g * DEC_MPAD + m;
+    const int g = warp / DEC_MPAD, m = warp % DEC_MPAD;
+    const size_t xi = act_xq_index(L.NG, L.G, m, g, 0);
+    uint8_t* dq = ws + A.xq_off + xi;
+    uint16_t* d16 = reinterpret_cast<uint16_t*>(ws + A.x16_off) + xi;
+    uint2* pdst = reinterpret_cast<uint2*>(ws + A.par_off) + (size_t)g * DEC_MPAD + m;
     const int b = (m < M) ? (row_bits ? row_bits[m0 + m] : bits) : 0;
-    if (b != 2 && b != 4 && b != 8) {
-        // padding row or BF16 bypass row: zero codes
-        if (b == 16) {  // still report non-finite inputs of bypass rows
-            const uint16_t* src = x + (size_t)(m0 + m) * L.K + (size_t)g * L.G;
-            for (int k = lane; k < L.G; k += 32)
-                if (!finite_f(bf16_bits_to_float(src[k])))
-                    report_nonfinite(err, (int64_t)(m0 + m) * L.K + (int64_t)g * L.G + k);
-        }
-        for (int k = lane; k < L.G; k += 32) dst[k] = 0;
-        if (lane == 0) *pdst = make_uint2(0u, 0u);
-        return;
-    }
     const uint16_t* src = x + (size_t)(m0 + m) * L.K + (size_t)g * L.G;
     constexpr int MAXV = 4;  // G <= 128
     float v[MAXV];
+    uint16_t raw[MAXV];
     float vmin = 0.f, vmax = 0.f;
     int bad = 0x7fffffff;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
         const int k = lane + 32 * i;
         v[i] = 0.f;
-        if (k < L.G) {
-            v[i] = bf16_bits_to_float(src[k]);
+        raw[i] = 0;
+        if (k < L.G && b != 0) {
+            raw[i] = src[k];
+            v[i] = bf16_bits_to_float(raw[i]);
             if (!finite_f(v[i])) bad = min(bad, k);
             vmin = fminf(vmin, v[i]);
             vmax = fmaxf(vmax, v[i]);
         }
     }
-    vmin = warp_min(vmin);
-    vmax = warp_max(vmax);
 #pragma unroll
     for (int o = 16; o; o >>= 1) bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
     if (bad != 0x7fffffff && lane == 0)
         report_nonfinite(err, (int64_t)(m0 + m) * L.K + (int64_t)g * L.G + bad);
+    if (b != 2 && b != 4 && b != 8) {  // padding row or BF16 bypass row
+#pragma unroll
+        for (int i = 0; i < MAXV; ++i) {
+            const int k = lane + 32 * i;
+            if (k < L.G) {
+                const int pos = (k & ~63) + dec_perm(k & 63);
+                dq[pos] = 0;
+                d16[pos] = (b == 16) ? raw[i] : (uint16_t)0;
+            }
+        }
+        if (lane == 0) *pdst = make_uint2(0u, 0u);
+        return;
+    }
+    vmin = warp_min(vmin);
+    vmax = warp_max(vmax);
     float s;
     int z;
     fit_params(vmin, vmax, b, &s, &z);
@@ -61,9 +72,9 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
         if (k < L.G) {
             const int q = quantize_one(v[i], s, z, b, L.round_mode);
             sum += q;
-            // 64-k sub-block permutation of the decode layout
             const int pos = (k & ~63) + dec_perm(k & 63);
-            dst[pos] = (uint8_t)q;
+            dq[pos] = (uint8_t)q;
+            d16[pos] = 0;
         }
     }
     sum = warp_sum_i(sum);
@@ -74,25 +85,33 @@ dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int
                                  int bits, void* ws, int64_t* err, cudaStream_t st) {
     // rows m0 .. m0+M-1 (M <= DEC_MPAD) of x / row_bits (base pointers)
     const ActLayoutDec A = act_layout_dec(L);
-    uint8_t* xq = reinterpret_cast<uint8_t*>(ws) + A.xq_off;
-    uint2* par = reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(ws) + A.par_off);
     const int warps = DEC_MPAD * L.NG;
-    actquant_dec_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(L, x, M, m0, row_bits, bits, xq, par, err);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((warps * 32 + 255) / 256);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, actquant_dec_kernel, L, x, M, m0, row_bits, bits,
+                                             reinterpret_cast<uint8_t*>(ws), A, err);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "actquant_dec_kernel launch: %s", cudaGetErrorString(e));
     return check_launch("actquant_dec_kernel");
 }
 
 // Test hook: export the decode-layout activation codes in logical layout.
-__global__ void actquant_export_kernel(WLayout L, int M, int m0, const uint8_t* __restrict__ xq,
-                                       const uint2* __restrict__ par, uint8_t* oq, float* os, uint8_t* oz,
-                                       int32_t* oSX) {
+__global__ void actquant_export_kernel(WLayout L, int M, int m0, const uint8_t* __restrict__ ws, ActLayoutDec A,
+                                       uint8_t* oq, float* os, uint8_t* oz, int32_t* oSX) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)M * L.K) return;
     const int m = (int)(idx / L.K), k = (int)(idx % L.K);
-    const int pos = (k & ~63) + dec_perm(k & 63);
-    oq[(size_t)(m0 + m) * L.K + k] = xq[(size_t)m * L.K + pos];
-    if (k % L.G == 0) {
-        const int g = k / L.G;
-        const uint2 p = par[(size_t)g * DEC_MPAD + m];
+    const int g = k / L.G, kk = k % L.G;
+    const int pos = (kk & ~63) + dec_perm(kk & 63);
+    oq[(size_t)(m0 + m) * L.K + k] = ws[A.xq_off + act_xq_index(L.NG, L.G, m, g, pos)];
+    if (kk == 0) {
+        const uint2 p = reinterpret_cast<const uint2*>(ws + A.par_off)[(size_t)g * DEC_MPAD + m];
         os[(size_t)(m0 + m) * L.NG + g] = __uint_as_float(p.x);
         oz[(size_t)(m0 + m) * L.NG + g] = (uint8_t)(p.y >> 16);
         oSX[(size_t)(m0 + m) * L.NG + g] = (int32_t)(p.y & 0xffffu);
@@ -104,8 +123,7 @@ dyq_status_t launch_actquant_export(const WLayout& L, int M, const void* ws, uin
     const ActLayoutDec A = act_layout_dec(L);
     const size_t total = (size_t)M * L.K;
     actquant_export_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
-        L, M, m0, reinterpret_cast<const uint8_t*>(ws) + A.xq_off,
-        reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(ws) + A.par_off), xq, sx, zx, SX);
+        L, M, m0, reinterpret_cast<const uint8_t*>(ws), A, xq, sx, zx, SX);
     return check_launch("actquant_export_kernel");
 }
 

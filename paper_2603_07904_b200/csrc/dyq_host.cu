@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <climits>
+#include <stdlib.h>
 
 #include "dyq_internal.cuh"
 
@@ -27,6 +28,11 @@ dyq_status_t check_launch(const char* what) {
     return DYQ_OK;
 }
 
+bool pdl_enabled() {
+    static const int off = getenv("DYQ_NO_PDL") ? atoi(getenv("DYQ_NO_PDL")) : 0;
+    return off == 0;
+}
+
 bool make_layout(const dyq_wdesc_t* wd, WLayout* L) {
     if (!wd) return false;
     L->N = wd->N;
@@ -41,18 +47,16 @@ bool make_layout(const dyq_wdesc_t* wd, WLayout* L) {
     L->nsub_last = (L->N - 128 * (L->T128 - 1)) / 16;
     L->chunk = 512 * (L->wbits / 4);
     L->codes_bytes = (size_t)L->N * L->K * L->wbits / 8;
-    const size_t slots = (size_t)L->T128 * L->NG * 128;
-    L->scales_bytes = slots * 4;
-    L->zeros_off = L->scales_bytes;
-    L->meta_bytes = L->scales_bytes + ((slots + 15) & ~(size_t)15);
+    L->meta_bytes = (size_t)L->T128 * L->NG * META_BLOCK;
     return true;
 }
 
 ActLayoutDec act_layout_dec(const WLayout& L) {
     ActLayoutDec A;
-    A.xq_off = 0;
-    A.par_off = ((size_t)DEC_MPAD * L.K + 255) & ~(size_t)255;
-    A.bytes = A.par_off + (((size_t)L.NG * DEC_MPAD * 8 + 255) & ~(size_t)255);
+    A.par_off = 0;
+    A.xq_off = ((size_t)L.NG * DEC_MPAD * 8 + 255) & ~(size_t)255;
+    A.x16_off = A.xq_off + (((size_t)DEC_MPAD * L.K + 255) & ~(size_t)255);
+    A.bytes = A.x16_off + (((size_t)DEC_MPAD * L.K * 2 + 255) & ~(size_t)255);
     return A;
 }
 
@@ -193,14 +197,17 @@ dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t tpe, const i
     return launch_route(bits, E, tpe, abits_of_host, row_bits, (cudaStream_t)stream);
 }
 
+// Workspace = [decode split-K accumulator + tile counters (must start zeroed;
+// self-cleaning)] [standalone activation-quantizer output (dyq_act_quant)].
+static size_t act_area_offset(const WLayout& L) { return (decode_ws_bytes(L) + 255) & ~(size_t)255; }
+
 dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* bytes) {
     WLayout L;
     dyq_status_t rc = validate_wdesc(wd, &L);
     if (rc) return rc;
     if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range [0, 65536]");
     if (!bytes) return set_error(DYQ_EINVAL, "null bytes");
-    const ActLayoutDec A = act_layout_dec(L);
-    *bytes = A.bytes;
+    *bytes = act_area_offset(L) + act_layout_dec(L).bytes;
     return DYQ_OK;
 }
 
@@ -211,29 +218,37 @@ dyq_status_t dyq_workspace_init(void* ws, size_t bytes, dyq_stream_t stream) {
     return DYQ_OK;
 }
 
-static dyq_status_t qlinear_common(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x,
-                                   int32_t M, const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype,
-                                   int32_t* I, void* ws, size_t ws_bytes, int64_t* err, cudaStream_t st) {
-    WLayout L;
-    dyq_status_t rc = validate_wdesc(wd, &L);
+static dyq_status_t validate_ql(const dyq_wdesc_t* wd, WLayout* L, const void* codes, const void* meta,
+                                const uint16_t* x, int32_t M, const int32_t* row_bits, int32_t bits, bool has_out,
+                                int32_t y_dtype, bool check_ydt, void* ws, size_t ws_bytes) {
+    dyq_status_t rc = validate_wdesc(wd, L);
     if (rc) return rc;
     if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range [0, 65536]");
     if (M == 0) return DYQ_OK;
-    if (!codes || !meta || !x || !ws || (!y && !I)) return set_error(DYQ_EINVAL, "null pointer");
+    if (!codes || !meta || !x || !ws || !has_out) return set_error(DYQ_EINVAL, "null pointer");
     if (!aligned16(codes) || !aligned16(meta) || !aligned16(ws) || !aligned16(x))
         return set_error(DYQ_EINVAL, "codes/meta/x/workspace must be 16-byte aligned");
     if (!row_bits && bits != 2 && bits != 4 && bits != 8 && bits != 16)
         return set_error(DYQ_EINVAL, "bits must be 2, 4, 8 or 16 (got %d)", bits);
-    if (y && y_dtype != 0 && y_dtype != 1) return set_error(DYQ_EINVAL, "y_dtype must be 0 (fp32) or 1 (bf16)");
+    if (check_ydt && y_dtype != 0 && y_dtype != 1) return set_error(DYQ_EINVAL, "y_dtype must be 0 (fp32) or 1 (bf16)");
     size_t need = 0;
     dyq_qlinear_workspace(wd, M, &need);
     if (ws_bytes < need) return set_error(DYQ_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, need);
-    // Decode path: 16-token tiles (the prefill kernel takes large M when built).
+    return DYQ_OK;
+}
+
+// Decode path: per 16-token tile, the activation quantizer writes the
+// workspace's activation area, then the decode kernel streams the weights
+// (programmatic dependent launch lets it start before the quantizer ends).
+static dyq_status_t run_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int32_t M,
+                               const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype, int32_t* I, void* ws,
+                               int64_t* err, cudaStream_t st) {
+    uint8_t* area = reinterpret_cast<uint8_t*>(ws) + act_area_offset(L);
     for (int m0 = 0; m0 < M; m0 += DEC_MPAD) {
         const int mt = (M - m0) < DEC_MPAD ? (M - m0) : DEC_MPAD;
-        rc = launch_actquant_dec(L, x, mt, m0, row_bits, bits, ws, err, st);
+        dyq_status_t rc = launch_actquant_dec(L, x, mt, m0, row_bits, bits, area, err, st);
         if (rc) return rc;
-        rc = launch_decode(L, codes, meta, x, mt, m0, M, row_bits, bits, y, y_dtype, I, ws, st);
+        rc = launch_decode(L, codes, meta, x, mt, m0, row_bits, bits, y, y_dtype, I, ws, err, st);
         if (rc) return rc;
     }
     return DYQ_OK;
@@ -242,17 +257,53 @@ static dyq_status_t qlinear_common(const dyq_wdesc_t* wd, const void* codes, con
 dyq_status_t dyq_qlinear(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x, int32_t M,
                          const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype, void* workspace,
                          size_t ws_bytes, int64_t* err, dyq_stream_t stream) {
-    if (!y && M > 0) return set_error(DYQ_EINVAL, "null y");
-    return qlinear_common(wd, codes, meta, x, M, row_bits, bits, y, y_dtype, nullptr, workspace, ws_bytes, err,
-                          (cudaStream_t)stream);
+    WLayout L;
+    dyq_status_t rc = validate_ql(wd, &L, codes, meta, x, M, row_bits, bits, y != nullptr, y_dtype, true, workspace,
+                                  ws_bytes);
+    if (rc || M == 0) return rc;
+    return run_decode(L, codes, meta, x, M, row_bits, bits, y, y_dtype, nullptr, workspace, err, (cudaStream_t)stream);
 }
 
 dyq_status_t dyq_qlinear_i32_partials(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x,
                                       int32_t M, const int32_t* row_bits, int32_t bits, int32_t* I, void* workspace,
                                       size_t ws_bytes, int64_t* err, dyq_stream_t stream) {
-    if (!I && M > 0) return set_error(DYQ_EINVAL, "null I");
-    return qlinear_common(wd, codes, meta, x, M, row_bits, bits, nullptr, 0, I, workspace, ws_bytes, err,
-                          (cudaStream_t)stream);
+    WLayout L;
+    dyq_status_t rc = validate_ql(wd, &L, codes, meta, x, M, row_bits, bits, I != nullptr, 0, false, workspace,
+                                  ws_bytes);
+    if (rc || M == 0) return rc;
+    return run_decode(L, codes, meta, x, M, row_bits, bits, nullptr, 0, I, workspace, err, (cudaStream_t)stream);
+}
+
+// Standalone quantizer into the workspace's activation area (inspection / reuse).
+dyq_status_t dyq_act_quant(const dyq_wdesc_t* wd, const uint16_t* x, int32_t M, const int32_t* row_bits,
+                           int32_t bits, void* ws, size_t ws_bytes, int64_t* err, dyq_stream_t stream) {
+    WLayout L;
+    dyq_status_t rc = validate_wdesc(wd, &L);
+    if (rc) return rc;
+    if (M < 0 || M > DEC_MPAD) return set_error(DYQ_EUNSUPPORTED, "dyq_act_quant supports M <= %d", DEC_MPAD);
+    if (M == 0) return DYQ_OK;
+    if (!x || !ws) return set_error(DYQ_EINVAL, "null pointer");
+    if (!aligned16(ws) || !aligned16(x)) return set_error(DYQ_EINVAL, "x/workspace must be 16-byte aligned");
+    if (!row_bits && bits != 2 && bits != 4 && bits != 8 && bits != 16)
+        return set_error(DYQ_EINVAL, "bits must be 2, 4, 8 or 16 (got %d)", bits);
+    size_t need = 0;
+    dyq_qlinear_workspace(wd, M, &need);
+    if (ws_bytes < need) return set_error(DYQ_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, need);
+    return launch_actquant_dec(L, x, M, 0, row_bits, bits, reinterpret_cast<uint8_t*>(ws) + act_area_offset(L), err,
+                               (cudaStream_t)stream);
+}
+
+// Linear layer on activations already quantized into `ws` by dyq_act_quant.
+dyq_status_t dyq_qlinear_q(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x,
+                           int32_t M, const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype, void* ws,
+                           size_t ws_bytes, dyq_stream_t stream) {
+    WLayout L;
+    dyq_status_t rc = validate_ql(wd, &L, codes, meta, x, M, row_bits, bits, y != nullptr, y_dtype, true, ws,
+                                  ws_bytes);
+    if (rc || M == 0) return rc;
+    if (M > DEC_MPAD) return set_error(DYQ_EUNSUPPORTED, "dyq_qlinear_q supports M <= %d", DEC_MPAD);
+    return launch_decode(L, codes, meta, x, M, 0, row_bits, bits, y, y_dtype, nullptr, ws, nullptr,
+                         (cudaStream_t)stream);
 }
 
 dyq_status_t dyq_act_quant_for_check(const dyq_wdesc_t* wd, const uint16_t* x, int32_t M, const int32_t* row_bits,
@@ -269,11 +320,12 @@ dyq_status_t dyq_act_quant_for_check(const dyq_wdesc_t* wd, const uint16_t* x, i
     dyq_qlinear_workspace(wd, M, &need);
     if (ws_bytes < need) return set_error(DYQ_EINVAL, "workspace too small");
     cudaStream_t st = (cudaStream_t)stream;
+    uint8_t* area = reinterpret_cast<uint8_t*>(ws) + act_area_offset(L);
     for (int m0 = 0; m0 < M; m0 += DEC_MPAD) {
         const int mt = (M - m0) < DEC_MPAD ? (M - m0) : DEC_MPAD;
-        rc = launch_actquant_dec(L, x, mt, m0, row_bits, bits, ws, err, st);
+        rc = launch_actquant_dec(L, x, mt, m0, row_bits, bits, area, err, st);
         if (rc) return rc;
-        rc = launch_actquant_export(L, mt, ws, xq, sx, zx, SX, m0, st);
+        rc = launch_actquant_export(L, mt, area, xq, sx, zx, SX, m0, st);
         if (rc) return rc;
     }
     return DYQ_OK;

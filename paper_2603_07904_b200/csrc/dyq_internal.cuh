@@ -26,10 +26,11 @@ namespace dyq {
 //         R2 = q[gid][16+4t..], R3 = q[gid+8][16+4t..] (k relative to the slab).
 //   Chunks are ordered (tile, slab pair, sub-tile) so that one (tile, slab pair)
 //   is 8 contiguous chunks (4 KB for W4) -- one bulk copy for the prefill kernel.
-// Metadata: scales fp32 then zero-points u8, each indexed
-//   ((tile * NG + g) * 8 + sub) * 16 + p,  p = 2 * (r % 8) + r / 8,
-//   r = row within the sub-tile: the decode lane of group gid reads the
-//   (row gid, row gid+8) pair with one 8-byte (scales) / 2-byte (zeros) load.
+// Metadata: one 640-byte block per (tile, group) -- 128 fp32 scales then 128
+//   u8 zero-points -- so a decode unit's metadata is one bulk copy.  Inside a
+//   block, row r of sub-tile `sub` sits at slot sub * 16 + p, p = 2 * (r % 8) +
+//   r / 8: the decode lane of group gid reads the (row gid, row gid+8) pair with
+//   one 8-byte (scales) / 2-byte (zeros) load.
 
 struct WLayout {
     int N, K, G, wbits, round_mode;
@@ -38,22 +39,30 @@ struct WLayout {
     int T128;     // ceil(N / 128)
     int nsub_last;
     int chunk;    // bytes per (tile, sp, sub) chunk
-    size_t codes_bytes, scales_bytes, zeros_off, meta_bytes;
+    size_t codes_bytes, meta_bytes;
 };
 
 __host__ __device__ inline size_t chunk_offset(const WLayout& L, int tile, int sp, int sub) {
     const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
     return ((size_t)tile * L.NSP * 8 + (size_t)sp * nsub + sub) * (size_t)L.chunk;
 }
-__host__ __device__ inline size_t meta_index(const WLayout& L, int tile, int g, int sub, int r) {
-    return (((size_t)tile * L.NG + g) * 8 + sub) * 16 + 2 * (r & 7) + (r >> 3);
+constexpr int META_BLOCK = 640;  // bytes of metadata per (tile, group)
+__host__ __device__ inline size_t meta_block(const WLayout& L, int tile, int g) {
+    return ((size_t)tile * L.NG + g) * META_BLOCK;
 }
+__host__ __device__ inline int meta_slot(int sub, int r) { return sub * 16 + 2 * (r & 7) + (r >> 3); }
 
-// Activation codes for the decode kernel: [Mpad = 16][K] u8, each 64-k group
-// permuted so that decode lane t reads its 4 B-fragment words with one 16-byte
-// load: position t*16 + s*8 + h*4 + b  <->  k = 32*s + 16*h + 4*t + b.
-// Per (group g, token m) parameters {float s_x; uint32 (z_x << 16) | SX}
-// at [g][Mpad][8 B] so that the lane owning tokens (2t, 2t+1) reads 16 B.
+// Activations for the decode kernel (<= 16 tokens, two halves of 8), laid out
+// so that a run of consecutive K-groups is contiguous in every array (one bulk
+// copy per array per pipeline stage):
+//   par [NG][16 tok] {float s_x; uint32 (z_x << 16) | SX}
+//   xq  [2 halves][NG][8 tok][G] u8 codes
+//   x16 [2 halves][NG][8 tok][G] bf16 copy of x for A16 (BF16-bypass) rows, else 0
+// Inside each 64-k block the k order is permuted so that decode lane t reads
+// all of its B-fragment words with 16-byte loads:
+//   position t*16 + s*8 + h*4 + b  <->  k = 32*s + 16*h + 4*t + b
+// (u8 codes: one 16-B load; bf16: two 16-B loads), and the lane owning C-tokens
+// (2t, 2t+1) reads both tokens' parameters with one 16-B load.
 constexpr int DEC_MPAD = 16;
 __host__ __device__ inline int dec_perm(int kk) {  // kk in [0,64) -> position
     const int s = kk >> 5, h = (kk >> 4) & 1, t = (kk >> 2) & 3, b = kk & 3;
@@ -61,8 +70,12 @@ __host__ __device__ inline int dec_perm(int kk) {  // kk in [0,64) -> position
 }
 
 struct ActLayoutDec {
-    size_t xq_off, par_off, bytes;
+    size_t par_off, xq_off, x16_off, bytes;
 };
+// element offsets of token m, group g, in-group position pos
+__host__ __device__ inline size_t act_xq_index(int NG, int G, int m, int g, int pos) {
+    return (((size_t)(m >> 3) * NG + g) * 8 + (m & 7)) * G + pos;
+}
 
 // ------------------------------------------------------------ error words
 __device__ inline void report_nonfinite(int64_t* err, int64_t idx) {
@@ -94,14 +107,30 @@ __device__ inline void fit_params(float vmin, float vmax, int bits, float* s_out
     *z_out = (int)zq;
 }
 
-// Eq. (2): q = clamp(floor(v / s) + z, 0, 2^b - 1), floor of the fp64 quotient of
-// the fp32 operands (exact for the in-range quotients, reading 4).
+// Exact floor(v / s) of the real quotient of two fp32 values (s > 0), in fp32:
+// an estimate from the correctly rounded reciprocal is off by at most one for
+// |v / s| < 2^20; the sign of each FMA remainder v - q s is exact (the FMA
+// rounds the exact value once, and a non-zero difference of these operands is
+// >= 2^-149, never flushed: no -ftz), so two checks make the floor exact.
+// Equal to the oracle's floor(fp64(v) / fp64(s)) (reading 4).
+__device__ __forceinline__ float floor_div_exact(float v, float s) {
+    float q = floorf(__fmul_rn(v, __frcp_rn(s)));
+    if (fmaf(-q, s, v) < 0.f) {
+        q -= 1.f;
+    } else if (fmaf(-(q + 1.f), s, v) >= 0.f) {
+        q += 1.f;
+    }
+    return q;
+}
+
+// Eq. (2): q = clamp(floor(v / s) + z, 0, 2^b - 1) with the exact floor;
+// round_mode 1: floor(v / s + 1/2), decided exactly from the sign of 2v - (2t+1)s.
 __device__ inline int quantize_one(float v, float s, int z, int bits, int round_mode) {
-    const double r = __ddiv_rn((double)v, (double)s);
-    double f = round_mode == 1 ? floor(__dadd_rn(r, 0.5)) : floor(r);
-    double c = f + (double)z;
-    const double levels = (double)((1 << bits) - 1);
-    c = c < 0.0 ? 0.0 : (c > levels ? levels : c);
+    float f = floor_div_exact(v, s);
+    if (round_mode == 1 && fmaf(-(2.f * f + 1.f), s, 2.f * v) >= 0.f) f += 1.f;
+    float c = f + (float)z;
+    const float levels = (float)((1 << bits) - 1);
+    c = c < 0.f ? 0.f : (c > levels ? levels : c);
     return (int)c;
 }
 
@@ -124,6 +153,7 @@ __device__ inline int warp_sum_i(int v) {
     return v;
 }
 
+size_t decode_ws_bytes(const WLayout& L);
 // dyq_select.cu
 size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
 dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);
@@ -136,6 +166,7 @@ dyq_status_t launch_route(const int32_t* bits, int32_t E, int32_t tpe, const int
 
 // host-side helpers (dyq_host.cu)
 namespace dyq {
+bool pdl_enabled();  // DYQ_NO_PDL=1 disables programmatic dependent launch (A/B timing)
 dyq_status_t set_error(dyq_status_t st, const char* fmt, ...);
 dyq_status_t check_launch(const char* what);
 bool make_layout(const dyq_wdesc_t* wd, WLayout* L);
@@ -150,10 +181,12 @@ dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int
                                  int bits, void* ws, int64_t* err, cudaStream_t st);
 dyq_status_t launch_actquant_export(const WLayout& L, int M, const void* ws, uint8_t* xq, float* sx,
                                     uint8_t* zx, int32_t* SX, int m0, cudaStream_t st);
-// rows m0 .. m0+M-1 (M <= DEC_MPAD); x, row_bits, y, I_out are base pointers
-dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x,
-                           int M, int m0, int Mtotal, const int32_t* row_bits, int bits, void* y,
-                           int y_dtype, int32_t* I_out, const void* ws, cudaStream_t st);
+// rows m0 .. m0+M-1 (M <= DEC_MPAD); x, row_bits, y, I_out are base pointers;
+// ws = zero-initialised split-K accumulator area (decode_ws_bytes)
+dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int M,
+                           int m0, const int32_t* row_bits, int bits, void* y, int y_dtype, int32_t* I_out,
+                           void* ws, int64_t* err, cudaStream_t st);
+size_t decode_ws_bytes(const WLayout& L);
 // dyq_select.cu
 size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
 dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);

@@ -6,8 +6,8 @@
 namespace dyq {
 
 // Phase 1: one warp per (row n, group g): exact min/max, fp64 fit -> meta.
-__global__ void pack_fit_kernel(WLayout L, const uint16_t* __restrict__ w, float* __restrict__ scales,
-                                uint8_t* __restrict__ zeros, int64_t* err) {
+__global__ void pack_fit_kernel(WLayout L, const uint16_t* __restrict__ w, uint8_t* __restrict__ meta,
+                                int64_t* err) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int total = L.N * L.NG;
@@ -32,15 +32,14 @@ __global__ void pack_fit_kernel(WLayout L, const uint16_t* __restrict__ w, float
         int z;
         fit_params(vmin, vmax, L.wbits, &s, &z);
         const int tile = n >> 7, sub = (n >> 4) & 7, r = n & 15;
-        const size_t mi = meta_index(L, tile, g, sub, r);
-        scales[mi] = s;
-        zeros[mi] = (uint8_t)z;
+        uint8_t* blk = meta + meta_block(L, tile, g);
+        reinterpret_cast<float*>(blk)[meta_slot(sub, r)] = s;
+        blk[512 + meta_slot(sub, r)] = (uint8_t)z;
     }
 }
 
 // Phase 2: one thread per 32-bit output word of the code layout.
-__global__ void pack_codes_kernel(WLayout L, const uint16_t* __restrict__ w,
-                                  const float* __restrict__ scales, const uint8_t* __restrict__ zeros,
+__global__ void pack_codes_kernel(WLayout L, const uint16_t* __restrict__ w, const uint8_t* __restrict__ meta,
                                   uint32_t* __restrict__ codes) {
     const size_t words = L.codes_bytes / 4;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -79,9 +78,9 @@ __global__ void pack_codes_kernel(WLayout L, const uint16_t* __restrict__ w,
     const int n = tile * 128 + sub * 16 + r;
     const int k0 = sp * 64 + slab * 32;  // slab start
     const int g = k0 / L.G;
-    const size_t mi = meta_index(L, tile, g, sub, r);
-    const float s = scales[mi];
-    const int z = zeros[mi];
+    const uint8_t* blk = meta + meta_block(L, tile, g);
+    const float s = reinterpret_cast<const float*>(blk)[meta_slot(sub, r)];
+    const int z = blk[512 + meta_slot(sub, r)];
     const uint16_t* src = w + (size_t)n * L.K;
     uint32_t word = 0;
     if (L.wbits == 4) {
@@ -103,23 +102,21 @@ __global__ void pack_codes_kernel(WLayout L, const uint16_t* __restrict__ w,
 
 dyq_status_t launch_pack(const WLayout& L, const uint16_t* w, void* codes, void* meta, int64_t* err,
                          cudaStream_t st) {
-    float* scales = reinterpret_cast<float*>(meta);
-    uint8_t* zeros = reinterpret_cast<uint8_t*>(meta) + L.zeros_off;
     // padded metadata slots of a ragged last tile stay deterministic
     cudaMemsetAsync(meta, 0, L.meta_bytes, st);
     const long long warps = (long long)L.N * L.NG;
-    pack_fit_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(L, w, scales, zeros, err);
+    pack_fit_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(L, w, reinterpret_cast<uint8_t*>(meta), err);
     dyq_status_t rc = check_launch("pack_fit_kernel");
     if (rc != DYQ_OK) return rc;
     const size_t words = L.codes_bytes / 4;
-    pack_codes_kernel<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(L, w, scales, zeros,
+    pack_codes_kernel<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(L, w, reinterpret_cast<const uint8_t*>(meta),
                                                                          reinterpret_cast<uint32_t*>(codes));
     return check_launch("pack_codes_kernel");
 }
 
 // Test hook: invert the layout (one thread per (n, k)).
-__global__ void unpack_kernel(WLayout L, const uint8_t* __restrict__ codes, const float* __restrict__ scales,
-                              const uint8_t* __restrict__ zeros, uint8_t* q, float* s, uint8_t* z) {
+__global__ void unpack_kernel(WLayout L, const uint8_t* __restrict__ codes, const uint8_t* __restrict__ meta,
+                              uint8_t* q, float* s, uint8_t* z) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)L.N * L.K) return;
     const int n = (int)(idx / L.K), k = (int)(idx % L.K);
@@ -141,9 +138,9 @@ __global__ void unpack_kernel(WLayout L, const uint8_t* __restrict__ codes, cons
     q[idx] = (uint8_t)val;
     if (k % L.G == 0) {
         const int g = k / L.G;
-        const size_t mi = meta_index(L, tile, g, sub, r);
-        s[(size_t)n * L.NG + g] = scales[mi];
-        z[(size_t)n * L.NG + g] = zeros[mi];
+        const uint8_t* blk = meta + meta_block(L, tile, g);
+        s[(size_t)n * L.NG + g] = reinterpret_cast<const float*>(blk)[meta_slot(sub, r)];
+        z[(size_t)n * L.NG + g] = blk[512 + meta_slot(sub, r)];
     }
 }
 
@@ -151,8 +148,7 @@ dyq_status_t launch_unpack(const WLayout& L, const void* codes, const void* meta
                            uint8_t* z, cudaStream_t st) {
     const size_t total = (size_t)L.N * L.K;
     unpack_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
-        L, reinterpret_cast<const uint8_t*>(codes), reinterpret_cast<const float*>(meta),
-        reinterpret_cast<const uint8_t*>(meta) + L.zeros_off, q, s, z);
+        L, reinterpret_cast<const uint8_t*>(codes), reinterpret_cast<const uint8_t*>(meta), q, s, z);
     return check_launch("unpack_kernel");
 }
 

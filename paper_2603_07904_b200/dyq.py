@@ -37,6 +37,8 @@ _SIGS = {
     "dyq_qlinear_i32_partials": [P, P, P, P, i32, P, i32, P, P, sz, P, P],
     "dyq_act_quant_for_check": [P, P, i32, P, i32, P, P, P, P, P, sz, P, P],
     "dyq_set_path": [i32],
+    "dyq_act_quant": [P, P, i32, P, i32, P, sz, P, P],
+    "dyq_qlinear_q": [P, P, P, P, i32, P, i32, P, i32, P, sz, P],
 }
 _RESTYPES = {"dyq_last_error": C.c_char_p, "dyq_version": C.c_char_p}
 
@@ -188,6 +190,17 @@ def qlinear(wd: WDesc, codes, meta, x, M: int, row_bits, bits: int, y, y_dtype: 
             err=None, stream=None):
     _call("dyq_qlinear", C.byref(wd), _ptr(codes), _ptr(meta), _ptr(x), M, _ptr(row_bits), bits,
           _ptr(y), y_dtype, _ptr(ws), ws.numel() * ws.element_size(), _ptr(err), _stream(stream))
+
+
+def act_quant(wd: WDesc, x, M: int, row_bits, bits: int, ws, err=None, stream=None):
+    _call("dyq_act_quant", C.byref(wd), _ptr(x), M, _ptr(row_bits), bits, _ptr(ws),
+          ws.numel() * ws.element_size(), _ptr(err), _stream(stream))
+
+
+def qlinear_q(wd: WDesc, codes, meta, x, M: int, row_bits, bits: int, y, y_dtype: int, ws,
+              stream=None):
+    _call("dyq_qlinear_q", C.byref(wd), _ptr(codes), _ptr(meta), _ptr(x), M, _ptr(row_bits), bits,
+          _ptr(y), y_dtype, _ptr(ws), ws.numel() * ws.element_size(), _stream(stream))
 
 
 def qlinear_i32_partials(wd: WDesc, codes, meta, x, M: int, row_bits, bits: int, I, ws,

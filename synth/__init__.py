@@ -71,6 +71,32 @@ def activations_bf16(M: int, K: int, seed: int, outlier_frac: float = 0.01,
     return f32_to_bf16_bits(x)
 
 
+def weights_bf16_torch(N: int, K: int, seed: int, device):
+    """Same recipe as weights_bf16, drawn on the device with torch (for the
+    full-size benchmark; values differ from the numpy draw, the recipe does not).
+    Returns an int16 tensor holding the bf16 bit patterns."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    row = torch.empty(N, 1, device=device).log_normal_(0.0, 0.5, generator=g)
+    w = torch.randn(N, K, device=device, generator=g) * 0.02 * row
+    return w.to(torch.bfloat16).view(torch.int16)
+
+
+def activations_bf16_torch(M: int, K: int, seed: int, device, outlier_frac: float = 0.01,
+                           outlier_scale: float = 20.0):
+    """Device draw of the activation recipe (int16 bf16 bit patterns)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    x = torch.randn(M, K, device=device, generator=g)
+    n_out = max(1, int(round(outlier_frac * K))) if outlier_frac > 0 else 0
+    if n_out:
+        ch = torch.randperm(K, device=device, generator=g)[:n_out]
+        x[:, ch] *= outlier_scale
+    return x.to(torch.bfloat16).view(torch.int16)
+
+
 _PHASES = ("transit", "align", "grasp", "place")
 
 
