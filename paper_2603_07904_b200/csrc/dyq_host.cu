@@ -200,6 +200,9 @@ dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t tpe, const i
 // Workspace = [decode split-K accumulator + tile counters (must start zeroed;
 // self-cleaning)] [standalone activation-quantizer output (dyq_act_quant)].
 static size_t act_area_offset(const WLayout& L) { return (decode_ws_bytes(L) + 255) & ~(size_t)255; }
+static size_t prefill_area_offset(const WLayout& L) {
+    return (act_area_offset(L) + act_layout_dec(L).bytes + 1023) & ~(size_t)1023;
+}
 
 dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* bytes) {
     WLayout L;
@@ -207,7 +210,7 @@ dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* byt
     if (rc) return rc;
     if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range [0, 65536]");
     if (!bytes) return set_error(DYQ_EINVAL, "null bytes");
-    *bytes = act_area_offset(L) + act_layout_dec(L).bytes;
+    *bytes = prefill_area_offset(L) + (M > DEC_MPAD ? pre_act_layout(L, M).bytes : 0);
     return DYQ_OK;
 }
 
@@ -243,6 +246,13 @@ static dyq_status_t validate_ql(const dyq_wdesc_t* wd, WLayout* L, const void* c
 static dyq_status_t run_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int32_t M,
                                const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype, int32_t* I, void* ws,
                                int64_t* err, cudaStream_t st) {
+    if (g_path == 2 || (g_path == 0 && M > DEC_MPAD)) {
+        // prefill: tcgen05 kernels over 128-token tiles
+        uint8_t* pa = reinterpret_cast<uint8_t*>(ws) + prefill_area_offset(L);
+        dyq_status_t rc = launch_actquant_pre(L, x, M, row_bits, bits, pa, err, st);
+        if (rc) return rc;
+        return launch_prefill(L, codes, meta, M, row_bits, bits, y, y_dtype, I, pa, st);
+    }
     uint8_t* area = reinterpret_cast<uint8_t*>(ws) + act_area_offset(L);
     for (int m0 = 0; m0 < M; m0 += DEC_MPAD) {
         const int mt = (M - m0) < DEC_MPAD ? (M - m0) : DEC_MPAD;

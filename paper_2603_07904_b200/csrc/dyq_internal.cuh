@@ -77,6 +77,16 @@ __host__ __device__ inline size_t act_xq_index(int NG, int G, int m, int g, int 
     return (((size_t)(m >> 3) * NG + g) * 8 + (m & 7)) * G + pos;
 }
 
+// Prefill activation operand (M > 16): per (128-token tile, K-group) the
+// UMMA canonical K-major no-swizzle blocks the tcgen05 kernel bulk-copies:
+//   codes [TT][NG][G/32 K-steps][144 rows][32 B]  (row 128 = all-ones column)
+//   x16   [TT][NG][G/16 K-steps][128 rows][16 bf16] (A16 rows, else 0)
+//   par   [TT][NG][128] {float s_x; uint32 (z_x << 16) | SX}
+struct PreActLayout {
+    size_t codes_off, x16_off, par_off, bytes;
+    size_t codes_group, x16_group;
+};
+
 // ------------------------------------------------------------ error words
 __device__ inline void report_nonfinite(int64_t* err, int64_t idx) {
     if (err) atomicMin(reinterpret_cast<unsigned long long*>(err), (unsigned long long)idx);
@@ -154,6 +164,12 @@ __device__ inline int warp_sum_i(int v) {
 }
 
 size_t decode_ws_bytes(const WLayout& L);
+PreActLayout pre_act_layout(const WLayout& L, int M);
+dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, const int32_t* row_bits, int bits,
+                                 void* act, int64_t* err, cudaStream_t st);
+dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,
+                            int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st);
+extern int g_path;
 // dyq_select.cu
 size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
 dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);
@@ -187,6 +203,12 @@ dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta
                            int m0, const int32_t* row_bits, int bits, void* y, int y_dtype, int32_t* I_out,
                            void* ws, int64_t* err, cudaStream_t st);
 size_t decode_ws_bytes(const WLayout& L);
+PreActLayout pre_act_layout(const WLayout& L, int M);
+dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, const int32_t* row_bits, int bits,
+                                 void* act, int64_t* err, cudaStream_t st);
+dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,
+                            int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st);
+extern int g_path;
 // dyq_select.cu
 size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
 dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);
