@@ -169,6 +169,11 @@ __device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&r)[16]) {
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
+__device__ __forceinline__ void ld8(uint32_t taddr, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void ld1(uint32_t taddr, uint32_t& r) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
 }
@@ -193,6 +198,9 @@ __host__ __device__ constexpr uint32_t idesc_i8_u8u8(int M, int N) {
            | (0u << 10)         /* B u8 */
            | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+__host__ __device__ constexpr uint32_t idesc_i8_s8s8(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
     return (1u << 4)            /* D format F32 */
            | (1u << 7)          /* A bf16 */
@@ -201,4 +209,26 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 }
 
 }  // namespace tc
+}  // namespace dyq
+
+namespace dyq {
+namespace ptx {
+// packed fp32x2 arithmetic (FMUL2 / FFMA2 on sm_100): d += a * b and r = a * b, lane-wise
+__device__ __forceinline__ void fma2f(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+    uint64_t d = ((uint64_t)__float_as_uint(d1) << 32) | __float_as_uint(d0);
+    const uint64_t a = ((uint64_t)__float_as_uint(a1) << 32) | __float_as_uint(a0);
+    const uint64_t b = ((uint64_t)__float_as_uint(b1) << 32) | __float_as_uint(b0);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+    d0 = __uint_as_float((uint32_t)d);
+    d1 = __uint_as_float((uint32_t)(d >> 32));
+}
+__device__ __forceinline__ void mul2f(float& r0, float& r1, float a0, float a1, float b0, float b1) {
+    uint64_t d;
+    const uint64_t a = ((uint64_t)__float_as_uint(a1) << 32) | __float_as_uint(a0);
+    const uint64_t b = ((uint64_t)__float_as_uint(b1) << 32) | __float_as_uint(b0);
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    r0 = __uint_as_float((uint32_t)d);
+    r1 = __uint_as_float((uint32_t)(d >> 32));
+}
+}  // namespace ptx
 }  // namespace dyq
