@@ -167,7 +167,7 @@ DYQ_API dyq_status_t dyq_workspace_init(void* workspace, size_t bytes, dyq_strea
  * y[m,n] = Sum_g s_w[n,g] Sum_{k in g} x[m,k] (q[n,k]-z_w[n,g]).
  *   x         device bf16 [M,K]
  *   row_bits  device int32 [M] (activation bits per token) or NULL -> `bits`
- *   y         device [M,N], y_dtype 0 = fp32, 1 = bf16
+ *   y         device [M,N] (16-byte aligned), y_dtype 0 = fp32, 1 = bf16
  *   workspace device buffer of dyq_qlinear_workspace() bytes (zeroed once)
  * One call reads the packed weights once for any mix of activation widths.
  * M in [0, 65536]; M <= 16 runs the bandwidth-bound decode kernel, larger M

@@ -271,6 +271,7 @@ dyq_status_t dyq_qlinear(const dyq_wdesc_t* wd, const void* codes, const void* m
     dyq_status_t rc = validate_ql(wd, &L, codes, meta, x, M, row_bits, bits, y != nullptr, y_dtype, true, workspace,
                                   ws_bytes);
     if (rc || M == 0) return rc;
+    if (!aligned16(y)) return set_error(DYQ_EINVAL, "y must be 16-byte aligned");
     return run_decode(L, codes, meta, x, M, row_bits, bits, y, y_dtype, nullptr, workspace, err, (cudaStream_t)stream);
 }
 

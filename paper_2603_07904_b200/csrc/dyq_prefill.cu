@@ -2,35 +2,42 @@
 // a warp-specialised tcgen05 GEMM with TMEM accumulators (sm_100a).
 //
 // "the packed activations ... utilize native INT4 and INT8
-// Tensor Cores"; "the computationally intensive visual prefill".  On
-// sm_100a there is no int4 MMA (tcgen05 .kind::i4 does not exist), so every
-// integer width runs on the 8-bit tensor pipe (tcgen05.mma .kind::i8 -> s32);
-// the BF16 bypass runs .kind::f16 (bf16 x bf16 -> f32).
+// Tensor Cores"; "the computationally intensive visual prefill".
 //
-// CTA = one 128-row weight tile x one 144-token tile (288 = 2 x 144: the
-// OpenVLA prefill of 256 vision + 32 text tokens tiles exactly), whole K:
+// Exact integer group sums on the bf16 tensor pipe.  Both operands are fed
+// CENTRED, as integers held in bf16:
+//     A[n][k] = q_w[n,k] - z_w[n,g]        |A| <= 255 (W8), <= 15 (W4)
+//     B[m][k] = Xq[m,k]  - z_x[m,g]        |B| <= 255 (A8), <= 15 (A4), <= 3 (A2)
+// Every integer of magnitude <= 256 is exact in bf16, every product is exact in
+// fp32 (16 significant bits), and a group sum is bounded by G * 255^2 <= 8.3e6
+// < 2^24, so tcgen05.mma .kind::f16 with an fp32 accumulator returns the exact
+// integer I[m,n,g] = Sum_k (Xq - z_x)(q - z_w) of Eq. (2)'s codes -- the value
+// the paper's INT4/INT8 tensor cores produce -- already as a float.  (The parity
+// tests check I bit-exactly, extreme A8 x W8 codes included.)  Why not
+// .kind::i8: with per-group scales on BOTH operands every group sum must be
+// promoted on the CUDA cores (acc += I * s_x * s_w per element and group); with
+// the s32 accumulator that costs an I2F per element plus a zero-point correction
+// for u8 operands, and those CUDA-core instructions -- not the tensor pipe --
+// bound the kernel.  The fp32 accumulator halves the promotion, and the bf16
+// pipe's rate (half of i8) stays above what the promotion can consume.
+// BF16-bypass tokens (A16) use the same MMA with B = x and s_x = 1, so
+// one pass serves any mix of activation widths in a token tile.
+//
+// CTA = one 128-row weight tile x one 144-token tile (288 = 2 x 144: the OpenVLA
+// prefill of 256 vision + 32 text tokens tiles exactly), whole K, 14 warps:
 //   warp 0      producer: per K-group, bulk copies (TMA engine) of the packed
-//               codes, the 640-B metadata block, the activation operand (already
-//               in the UMMA canonical K-major layout, written by the prefill
-//               activation quantizer) and the token scales;
-//   warp 1      MMA issuer (one thread): tcgen05.mma per 32-B K step into a
-//               double-buffered TMEM accumulator (one buffer per group);
-//   warps 2-3   transform: packed int4 -> 8-bit (or bf16 (q - z_w)) operand in
-//               the canonical no-swizzle K-major layout;
-//   warps 4-11  promotion: tcgen05.ld the group's sums, scale by s_x s_w and
-//               accumulate fp32 in registers; store y at the end.
-//
-// Zero points: when the weights are W4 and no token of the
-// tile runs at 8 bits, BOTH operands are centred -- A = q - z_w (transform) and
-// B = Xq - z_x (quantizer), each in [-15, 15] -- so the s8 x s8 MMA yields the
-// exact group sum I = Sum (Xq - z_x)(q - z_w) directly and the promotion is only
-// acc += float(I) * s_x * s_w (INTC mode).  Otherwise (A8 or W8 operands do not
-// fit s8) u8 x u8 codes are multiplied and the promotion applies
-//     I = P - z_w SX - z_x (Sum q - G z_w)
-// with Sum q taken from an all-ones token column of the MMA (INTU mode).
-// The per-group promotion is intrinsic to per-group scales on both operands: it
-// bounds the tensor pipe to roughly G / (64 c) of peak for c CUDA-core
-// instructions per accumulator element (c ~ 2.25 in INTC mode).
+//               codes, the 640-B metadata block, the B operand (already in the
+//               UMMA canonical K-major layout, written by the prefill quantizer)
+//               and the token scales into an smem ring;
+//   warp 1      MMA issuer (one thread): G/16 tcgen05.mma per group, A from
+//               TMEM, B from smem, into a double-buffered TMEM accumulator;
+//   warps 2-5   transform: packed codes -> bf16 (q - z_w), written straight to
+//               TMEM with tcgen05.st.16x256b (the packed lane-fragment order IS
+//               the 16x256b register fragment), so the A operand never touches
+//               shared memory;
+//   warps 6-13  promotion: tcgen05.ld.16x256b the group's sums, acc += D s_x s_w
+//               (FMUL2 + FFMA2) in registers; transposed 16-B stores at the end.
+// TMEM columns: [0,144) [144,288) accumulators, then NA A-operand buffers.
 #include <stdlib.h>
 
 #include "dyq_internal.cuh"
@@ -38,11 +45,13 @@
 
 namespace dyq {
 
-constexpr int PT = 144;   // real tokens per token tile
-constexpr int PTE = 160;  // operand rows in the code layout (row 144 = all-ones column)
-constexpr int PRE_WARPS = 12;
+constexpr int PT = 144;  // tokens per token tile (MMA N)
+constexpr int PRE_WARPS = 14;
 constexpr int PRE_THREADS = PRE_WARPS * 32;
-constexpr int PAR_BYTES = PT * 8;  // per (tile, group): float s_x[144] then uint32 (z_x<<16|SX)[144]
+constexpr int PAR_BYTES = PT * 4;  // per (tile, group): float s_x[144] (1 for A16 tokens, 0 for absent)
+constexpr int XF_WARPS = 4;
+constexpr int PR_WARP0 = 2 + XF_WARPS;  // first promotion warp
+constexpr uint32_t ACC_COLS = 2 * PT;   // TMEM: two 144-column accumulators, then the A buffers
 
 struct PreArgs {
     WLayout L;
@@ -60,20 +69,15 @@ struct PreArgs {
     int off_meta, off_b, off_par, off_a;
 };
 
-enum { PMODE_INTC = 0, PMODE_INTU = 1, PMODE_BF16 = 2 };
-
 __device__ __forceinline__ int token_bits(const PreArgs& a, int m) { return a.row_bits ? a.row_bits[m] : a.bits; }
 
-// tile flags: bit0 int tokens, bit1 A16 tokens, bit2 A8 tokens
-__device__ __forceinline__ int tile_flags_from_bits(int b) { return b == 16 ? 2 : (b == 8 ? 5 : 1); }
-
-template <int WBITS, int SPG, int MODE, bool PARTIALS>
+template <int WBITS, int SPG, bool PARTIALS>
 __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const PreArgs a) {
     constexpr int G = SPG * 64;
-    constexpr bool INT = MODE != PMODE_BF16;
-    constexpr int KSTEPS = INT ? G / 32 : G / 16;                     // MMA K steps per group
-    constexpr int NMMA = MODE == PMODE_INTU ? PTE : PT;               // MMA N
-    constexpr uint32_t BSTEP = INT ? PTE * 32 : PT * 32;              // bytes per K step of B in smem
+    constexpr int KSTEPS = G / 16;         // bf16 MMA K steps per group
+    constexpr uint32_t BSTEP = PT * 32;    // B bytes per K step
+    constexpr int NA = SPG == 1 ? 6 : 3;   // A-operand buffers in TMEM
+    constexpr uint32_t A_COLS = 8 * KSTEPS;
     const WLayout& L = a.L;
     const int tile = blockIdx.x, tt = blockIdx.y;
     const int NG = L.NG;
@@ -83,39 +87,31 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* xformed = full + S;
-    uint64_t* empty = xformed + S;
+    uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;   // [2]
     uint64_t* tempty = tfull + 2;  // [2]
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
-    int* s_flags = reinterpret_cast<int*>(s_tmem + 1);
+    uint64_t* afull = tempty + 2;  // [NA]
+    uint64_t* aempty = afull + NA; // [NA]
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(aempty + NA);
+    uint8_t* s_col = smem + 512;  // per token column: 0 absent, 1 integer bits, 2 BF16 bypass
     uint8_t* stage0 = smem + 1024;
 
-    // which kinds of tokens live in this token tile? (same rule as the quantizer)
-    if (threadIdx.x == 0) *s_flags = 0;
-    __syncthreads();
     for (int i = threadIdx.x; i < PT; i += PRE_THREADS) {
         const int m = tt * PT + i;
-        if (m < a.M) atomicOr(s_flags, tile_flags_from_bits(token_bits(a, m)));
+        s_col[i] = m < a.M ? (token_bits(a, m) == 16 ? 2 : 1) : 0;
     }
-    __syncthreads();
-    const int flags = *s_flags;
-    const bool centred = (L.wbits == 4) && !(flags & 4);
-    bool run;
-    if (PARTIALS) run = flags != 0 && (MODE == PMODE_INTC ? centred : !centred);
-    else if (MODE == PMODE_BF16) run = (flags & 2) != 0;
-    else run = (flags & 1) && (MODE == PMODE_INTC ? centred : !centred);
-    if (!run) return;
-
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&xformed[s], 2);    // 2 transform warps
-            ptx::mbar_init(&empty[s], 1 + 8);  // MMA commit + 8 promotion warps
+            ptx::mbar_init(&empty[s], 1 + 8 + XF_WARPS);  // MMA commit + promotion + transform warps
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&tfull[b], 1);
             ptx::mbar_init(&tempty[b], 8);
+        }
+        for (int i = 0; i < NA; ++i) {
+            ptx::mbar_init(&afull[i], XF_WARPS);
+            ptx::mbar_init(&aempty[i], 1);
         }
         ptx::fence_mbar_init();
     }
@@ -134,229 +130,247 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
         if (lane == 0) {
             const uint32_t cbytes = (uint32_t)(SPG * nsub * L.chunk);
             const uint32_t bbytes = KSTEPS * BSTEP;
+            int s = 0;
+            uint32_t ph = 0;
             for (int g = 0; g < NG; ++g) {
-                const int s = g % S;
-                if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+                if (g >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
                 ptx::mbar_arrive_expect_tx(&full[s], cbytes + META_BLOCK + bbytes + PAR_BYTES);
                 ptx::bulk_g2s(st, a.codes + chunk_offset(L, tile, g * SPG, 0), cbytes, &full[s]);
                 ptx::bulk_g2s(st + a.off_meta, a.meta + meta_block(L, tile, g), META_BLOCK, &full[s]);
                 const size_t tg = (size_t)tt * NG + g;
-                if (INT)
-                    ptx::bulk_g2s(st + a.off_b, a.act + a.P.codes_off + tg * a.P.codes_group, bbytes, &full[s]);
-                else
-                    ptx::bulk_g2s(st + a.off_b, a.act + a.P.x16_off + tg * a.P.x16_group, bbytes, &full[s]);
+                ptx::bulk_g2s(st + a.off_b, a.act + a.P.x16_off + tg * a.P.x16_group, bbytes, &full[s]);
                 ptx::bulk_g2s(st + a.off_par, a.act + a.P.par_off + tg * PAR_BYTES, PAR_BYTES, &full[s]);
+                if (++s == S) { s = 0; ph ^= 1; }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer
-        const uint32_t idesc = MODE == PMODE_INTC   ? tc::idesc_i8_s8s8(128, NMMA)
-                               : MODE == PMODE_INTU ? tc::idesc_i8_u8u8(128, NMMA)
-                                                    : tc::idesc_bf16(128, NMMA);
+        constexpr uint32_t idesc = tc::idesc_bf16(128, PT);
+        int s = 0, ai = 0;
+        uint32_t ph = 0, aph = 0;
         for (int g = 0; g < NG; ++g) {
-            const int s = g % S, b = g & 1;
-            ptx::mbar_wait(&xformed[s], (g / S) & 1);
+            const int b = g & 1;
+            ptx::mbar_wait(&full[s], ph);      // B operand landed
+            ptx::mbar_wait(&afull[ai], aph);   // A operand written to TMEM
             if (g >= 2) ptx::mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
             tc::fence_after();
             if (lane == 0) {
                 const uint32_t st = sbase + s * a.stage_bytes;
-                const uint32_t d = tmem + b * 256;
+                const uint32_t d = tmem + b * PT;
+                const uint32_t at = tmem + ACC_COLS + ai * A_COLS;
 #pragma unroll
                 for (int ks = 0; ks < KSTEPS; ++ks) {
-                    const uint64_t ad = tc::smem_desc(st + a.off_a + ks * 4096, 128, 256);
                     const uint64_t bd = tc::smem_desc(st + a.off_b + ks * BSTEP, 128, 256);
-                    if (INT)
-                        tc::mma_i8(d, ad, bd, idesc, ks > 0);
-                    else
-                        tc::mma_f16(d, ad, bd, idesc, ks > 0);
+                    tc::mma_f16_ta(d, at + ks * 8, bd, idesc, ks > 0);
                 }
                 tc::commit(ptx::smem_u32(&tfull[b]));
                 tc::commit(ptx::smem_u32(&empty[s]));
+                tc::commit(ptx::smem_u32(&aempty[ai]));
             }
             __syncwarp();
+            if (++s == S) { s = 0; ph ^= 1; }
+            if (++ai == NA) { ai = 0; aph ^= 1; }
         }
-    } else if (warp < 4) {
+    } else if (warp < PR_WARP0) {
         // ------------------------------------------------------ transform
-        const int tid = threadIdx.x - 64;  // 0..63
+        // Warp with TMEM quadrant q writes the A rows of sub-tiles 2q and 2q+1
+        // (TMEM lanes 32q.. and 32q+16..).  Lane (gid, t) owns lane-chunk
+        // (gid, t) of each sub-tile: rows gid and gid+8, k = 4t..4t+3 of every K
+        // step -- exactly the 16x256b register fragment, so each sub-tile and
+        // slab pair is one LDS.128 and one tcgen05.st.16x256b.x4.
+        const int q = warp & 3;
+        int s = 0, ai = 0;
+        uint32_t ph = 0, aph = 0;
         for (int g = 0; g < NG; ++g) {
-            const int s = g % S;
-            ptx::mbar_wait(&full[s], (g / S) & 1);
-            uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
-            uint8_t* A = st + a.off_a;
+            ptx::mbar_wait(&full[s], ph);
+            if (g >= NA) ptx::mbar_wait(&aempty[ai], aph ^ 1);
+            tc::fence_after();
+            const uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
             const uint8_t* zrow = st + a.off_meta + 512;
-            if (WBITS == 4) {
-                // SPG * nsub * 32 lane-chunks of 16 B: [spi][sub][lane]
-                for (int c = tid; c < SPG * nsub * 32; c += 64) {
-                    const int spi = c / (nsub * 32), cc = c - spi * nsub * 32;
-                    const int sub = cc >> 5, ln = cc & 31;
-                    const int gid = ln >> 2, t = ln & 3;
-                    const uint4 w = *reinterpret_cast<const uint4*>(st + c * 16);
-                    const uint32_t ws4[4] = {w.x, w.y, w.z, w.w};  // (slab0,r0) (slab0,r1) (slab1,r0) (slab1,r1)
+            const uint32_t at = tmem + ACC_COLS + ai * A_COLS;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int slab = j >> 1, r = sub * 16 + gid + 8 * (j & 1);
-                        uint32_t lo = ws4[j] & 0x0F0F0F0Fu, hi = (ws4[j] >> 4) & 0x0F0F0F0Fu;
-                        if (MODE == PMODE_INTC) {
-                            // s8 (q - z_w): (128 + q - z) per byte never borrows, then flip the sign bit
-                            const uint32_t zz = (uint32_t)zrow[meta_slot(sub, r & 15)] * 0x01010101u;
-                            lo = ((lo | 0x80808080u) - zz) ^ 0x80808080u;
-                            hi = ((hi | 0x80808080u) - zz) ^ 0x80808080u;
-                        }
-                        if (INT) {
-                            uint8_t* p = A + (spi * 2 + slab) * 4096 + (r >> 3) * 256 + (r & 7) * 16 + 4 * t;
-                            *reinterpret_cast<uint32_t*>(p) = lo;
-                            *reinterpret_cast<uint32_t*>(p + 128) = hi;
-                        } else {
-                            const uint32_t zw = zrow[meta_slot(sub, r & 15)];
-                            const uint32_t zz = 0x43004300u | (zw << 16) | zw;
+            for (int si = 0; si < 2; ++si) {
+                const int sub = 2 * q + si;
+                if (sub >= nsub) break;
+                const uint32_t tl = at + ((uint32_t)(32 * q + 16 * si) << 16);
+                // zero points of rows gid and gid+8 are adjacent metadata slots
+                const uint32_t z01 = *reinterpret_cast<const uint16_t*>(zrow + sub * 16 + 2 * (lane >> 2));
+                if (WBITS == 4) {
+                    // bf16 (128 + z) pairs; 0x43XX is exactly 128 + XX for XX < 128
+                    const uint32_t zz0 = 0x43004300u | ((z01 & 0xffu) * 0x00010001u);
+                    const uint32_t zz1 = 0x43004300u | ((z01 >> 8) * 0x00010001u);
+#pragma unroll
+                    for (int spi = 0; spi < SPG; ++spi) {
+                        // W4 chunk words: (slab0,r0) (slab0,r1) (slab1,r0) (slab1,r1);
+                        // byte i: k = 32 slab + 4t + i (low nibble), +16 (high nibble)
+                        const uint4 wv = *reinterpret_cast<const uint4*>(st + ((spi * nsub + sub) * 32 + lane) * 16);
+                        const uint32_t ws4[4] = {wv.x, wv.y, wv.z, wv.w};
+                        uint32_t r[16];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int slab = j >> 1, rs = j & 1;
+                            const uint32_t zz = rs ? zz1 : zz0;
                             const __nv_bfloat162 z2 = *reinterpret_cast<const __nv_bfloat162*>(&zz);
-                            const uint32_t plo0 = __byte_perm(lo, 0x4343u, 0x5140u), plo1 = __byte_perm(lo, 0x4343u, 0x5342u);
-                            const uint32_t phi0 = __byte_perm(hi, 0x4343u, 0x5140u), phi1 = __byte_perm(hi, 0x4343u, 0x5342u);
-                            __nv_bfloat162 t0 = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&plo0), z2);
-                            __nv_bfloat162 t1 = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&plo1), z2);
-                            __nv_bfloat162 t2 = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&phi0), z2);
-                            __nv_bfloat162 t3 = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&phi1), z2);
-                            // lo nibbles: k = 32*slab + 4t + b -> K step 4*spi + 2*slab, hi: +1
-                            const int ks = spi * 4 + slab * 2;
-                            const int off = (r >> 3) * 256 + (t >> 1) * 128 + (r & 7) * 16 + (t & 1) * 8;
-                            *reinterpret_cast<uint2*>(A + ks * 4096 + off) =
-                                make_uint2(*reinterpret_cast<uint32_t*>(&t0), *reinterpret_cast<uint32_t*>(&t1));
-                            *reinterpret_cast<uint2*>(A + (ks + 1) * 4096 + off) =
-                                make_uint2(*reinterpret_cast<uint32_t*>(&t2), *reinterpret_cast<uint32_t*>(&t3));
+                            const uint32_t lo = ws4[j] & 0x0F0F0F0Fu, hi = (ws4[j] >> 4) & 0x0F0F0F0Fu;
+                            const uint32_t p[4] = {__byte_perm(lo, 0x4343u, 0x5140u), __byte_perm(lo, 0x4343u, 0x5342u),
+                                                   __byte_perm(hi, 0x4343u, 0x5140u), __byte_perm(hi, 0x4343u, 0x5342u)};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const __nv_bfloat162 d2 = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&p[u]), z2);
+                                // K step 2 slab + (u>>1) (high nibbles: +1), register (rows gid / gid+8, pair u&1)
+                                r[(2 * slab + (u >> 1)) * 4 + rs * 2 + (u & 1)] = *reinterpret_cast<const uint32_t*>(&d2);
+                            }
                         }
+                        tc::st16x256_x4(tl + spi * 32, r);
                     }
-                }
-            } else {
-                // W8: [spi][sub][slab][lane][16 B = R0 R1 R2 R3]
-                for (int c = tid; c < SPG * nsub * 64; c += 64) {
-                    const int spi = c / (nsub * 64), cc = c - spi * nsub * 64;
-                    const int sub = cc >> 6, slab = (cc >> 5) & 1, ln = cc & 31;
-                    const int gid = ln >> 2, t = ln & 3;
-                    const uint4 w = *reinterpret_cast<const uint4*>(st + c * 16);
-                    const uint32_t R[4] = {w.x, w.y, w.z, w.w};  // (r0,h0) (r1,h0) (r0,h1) (r1,h1)
+                } else {
+                    const float zf0 = 8388608.f + (float)(z01 & 0xffu), zf1 = 8388608.f + (float)(z01 >> 8);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int r = sub * 16 + gid + 8 * (j & 1), h = j >> 1;
-                        if (INT) {
-                            uint8_t* p = A + (spi * 2 + slab) * 4096 + (r >> 3) * 256 + h * 128 + (r & 7) * 16 + 4 * t;
-                            *reinterpret_cast<uint32_t*>(p) = R[j];
-                        } else {
-                            const float zf = 8388608.f + (float)zrow[meta_slot(sub, r & 15)];
-                            float f[4];
+                    for (int spi = 0; spi < SPG; ++spi) {
+                        uint32_t r[16];
 #pragma unroll
-                            for (int bb = 0; bb < 4; ++bb)
-                                f[bb] = __uint_as_float(__byte_perm(R[j], 0x4B000000u, 0x7540u + bb)) - zf;
-                            __nv_bfloat162 p0 = __floats2bfloat162_rn(f[0], f[1]);
-                            __nv_bfloat162 p1 = __floats2bfloat162_rn(f[2], f[3]);
-                            const int ks = spi * 4 + slab * 2 + h;
-                            const int off = (r >> 3) * 256 + (t >> 1) * 128 + (r & 7) * 16 + (t & 1) * 8;
-                            *reinterpret_cast<uint2*>(A + ks * 4096 + off) =
-                                make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
+                        for (int slab = 0; slab < 2; ++slab) {
+                            // W8 chunk words: (r0,h0) (r1,h0) (r0,h1) (r1,h1); byte i: k = 32 slab + 16 h + 4t + i
+                            const uint4 wq = *reinterpret_cast<const uint4*>(
+                                st + (((spi * nsub + sub) * 2 + slab) * 32 + lane) * 16);
+                            const uint32_t R[4] = {wq.x, wq.y, wq.z, wq.w};
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const int rs = j & 1, hh = j >> 1;
+                                const float zf = rs ? zf1 : zf0;
+                                float f[4];
+#pragma unroll
+                                for (int bb = 0; bb < 4; ++bb)  // (2^23 + byte) - (2^23 + z): exact q - z
+                                    f[bb] = __uint_as_float(__byte_perm(R[j], 0x4B000000u, 0x7540u + bb)) - zf;
+                                __nv_bfloat162 p0 = __floats2bfloat162_rn(f[0], f[1]);
+                                __nv_bfloat162 p1 = __floats2bfloat162_rn(f[2], f[3]);
+                                const int ks = 2 * slab + hh;
+                                r[ks * 4 + rs * 2 + 0] = *reinterpret_cast<uint32_t*>(&p0);
+                                r[ks * 4 + rs * 2 + 1] = *reinterpret_cast<uint32_t*>(&p1);
+                            }
                         }
+                        tc::st16x256_x4(tl + spi * 32, r);
                     }
                 }
             }
-            tc::fence_proxy_async_smem();  // generic smem writes -> async proxy (MMA operand)
+            tc::wait_st();
+            tc::fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&xformed[s]);
+            if (lane == 0) {
+                ptx::mbar_arrive(&afull[ai]);
+                ptx::mbar_arrive(&empty[s]);
+            }
+            if (++s == S) { s = 0; ph ^= 1; }
+            if (++ai == NA) { ai = 0; aph ^= 1; }
         }
     } else {
         // ------------------------------------------------------ promotion
-        const int e = warp - 4;      // 0..7
-        const int q = warp & 3;      // TMEM lane quadrant (hardware: warp id % 4)
-        const int h = e >> 2;        // column half: tokens [72h, 72h + 72)
-        const int r = q * 32 + lane;  // weight row in the tile = TMEM lane
-        const int sub = r >> 4, rr = r & 15;
-        constexpr int NC = PT / 2;   // 72 columns per thread
-        float facc[NC];
+        // 16x256b loads: thread (gid, t) holds rows 32q + 16 si + gid (+8) and
+        // columns 8 blk + 2t, 2t+1 -- each thread needs only 18 of the 72 s_x.
+        const int e = warp - PR_WARP0;  // 0..7
+        const int q = warp & 3;         // TMEM lane quadrant (hardware: warp id % 4)
+        const int h = e >> 2;           // column half: tokens [72h, 72h + 72)
+        const int gid = lane >> 2, t = lane & 3;
+        constexpr int NC = PT / 2;      // 72 columns per warp
+        constexpr int NB = NC / 8;      // 9 column blocks
+        float facc[NB * 8];             // [blk][si][j]
 #pragma unroll
-        for (int c = 0; c < NC; ++c) facc[c] = 0.f;
+        for (int c = 0; c < NB * 8; ++c) facc[c] = 0.f;
+        int s = 0;
         for (int g = 0; g < NG; ++g) {
-            const int s = g % S, b = g & 1;
+            const int b = g & 1;
             ptx::mbar_wait(&tfull[b], (g >> 1) & 1);
             tc::fence_after();
             const uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
-            const float sw = reinterpret_cast<const float*>(st + a.off_meta)[meta_slot(sub, rr)];
-            const int zw = st[a.off_meta + 512 + meta_slot(sub, rr)];
-            const float* sxp = reinterpret_cast<const float*>(st + a.off_par) + h * NC;
-            const uint32_t* cxp = reinterpret_cast<const uint32_t*>(st + a.off_par + PT * 4) + h * NC;
-            const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + b * 256;
-            int T = 0;
-            if (MODE == PMODE_INTU) {
-                uint32_t sq;
-                tc::ld1(tb + PT, sq);
-                tc::wait_ld();
-                T = (int)sq - G * zw;
-            }
+            const float* swp = reinterpret_cast<const float*>(st + a.off_meta);
+            const float2 sw0 = *reinterpret_cast<const float2*>(swp + (2 * q) * 16 + 2 * gid);      // sub 2q
+            const float2 sw1 = *reinterpret_cast<const float2*>(swp + (2 * q + 1) * 16 + 2 * gid);  // sub 2q+1
+            const float* sxp = reinterpret_cast<const float*>(st + a.off_par) + h * NC + 2 * t;
+            const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + b * PT + h * NC;
+            auto promote = [&](const uint32_t* v, int nblk, int blk0) {
 #pragma unroll
-            for (int c0 = 0; c0 < NC; c0 += 24) {
-                uint32_t v[24];
-                tc::ld8(tb + h * NC + c0, &v[0]);
-                tc::ld8(tb + h * NC + c0 + 8, &v[8]);
-                tc::ld8(tb + h * NC + c0 + 16, &v[16]);
-                tc::wait_ld();
-                if (c0 + 24 == NC) {  // all columns of this buffer are in registers
-                    tc::fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&tempty[b]);
-                }
+                for (int bi = 0; bi < nblk; ++bi) {
+                    const float2 sx = *reinterpret_cast<const float2*>(sxp + (blk0 + bi) * 8);
 #pragma unroll
-                for (int c = 0; c < 24; c += 4) {
-                    const float4 sx4 = *reinterpret_cast<const float4*>(sxp + c0 + c);
-                    const float sxv[4] = {sx4.x, sx4.y, sx4.z, sx4.w};
-                    int I[4];
-                    if (MODE == PMODE_INTU) {
-                        const uint4 cx4 = *reinterpret_cast<const uint4*>(cxp + c0 + c);
-                        const uint32_t cxv[4] = {cx4.x, cx4.y, cx4.z, cx4.w};
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            I[k] = (int)v[c + k] - zw * (int)(cxv[k] & 0xffffu) - (int)(cxv[k] >> 16) * T;
-                    } else if (INT) {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) I[k] = (int)v[c + k];
+                    for (int si = 0; si < 2; ++si) {
+                        const uint32_t* vv = v + si * 4 * nblk + bi * 4;
+                        const float2 sw = si ? sw1 : sw0;
+                        float* fa = facc + ((blk0 + bi) * 2 + si) * 4;
+                        float t0, t1, t2, t3;
+                        ptx::mul2f(t0, t1, __uint_as_float(vv[0]), __uint_as_float(vv[1]), sx.x, sx.y);
+                        ptx::mul2f(t2, t3, __uint_as_float(vv[2]), __uint_as_float(vv[3]), sx.x, sx.y);
+                        ptx::fma2f(fa[0], fa[1], t0, t1, sw.x, sw.x);
+                        ptx::fma2f(fa[2], fa[3], t2, t3, sw.y, sw.y);
                     }
-                    if constexpr (PARTIALS) {
+                }
+            };
+            auto partials = [&](const uint32_t* v, int nblk, int blk0) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const int m = tt * PT + h * NC + c0 + c + k;
-                            if (m < a.M && r < nsub * 16)
+                for (int bi = 0; bi < nblk; ++bi)
+#pragma unroll
+                    for (int si = 0; si < 2; ++si)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int r = 32 * q + 16 * si + gid + 8 * (j >> 1);
+                            const int cl = h * NC + (blk0 + bi) * 8 + 2 * t + (j & 1), m = tt * PT + cl;
+                            const int cf = s_col[cl];
+                            if (cf != 0 && r < nsub * 16)
                                 a.I_out[((size_t)m * L.N + tile * 128 + r) * NG + g] =
-                                    token_bits(a, m) == 16 ? 0 : I[k];
+                                    cf == 2 ? 0 : __float2int_rn(__uint_as_float(v[si * 4 * nblk + bi * 4 + j]));
                         }
-                    } else if (INT) {
+            };
 #pragma unroll
-                        for (int k = 0; k < 4; k += 2) {
-                            float t0, t1;
-                            ptx::mul2f(t0, t1, (float)I[k], (float)I[k + 1], sxv[k], sxv[k + 1]);
-                            ptx::fma2f(facc[c0 + c + k], facc[c0 + c + k + 1], t0, t1, sw, sw);
-                        }
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 4; k += 2)
-                            ptx::fma2f(facc[c0 + c + k], facc[c0 + c + k + 1], __uint_as_float(v[c + k]),
-                                     __uint_as_float(v[c + k + 1]), sw, sw);
-                    }
-                }
+            for (int c = 0; c < 2; ++c) {  // blocks 0-3, 4-7
+                uint32_t v[32];
+                tc::ld16x256_x4(tb + c * 32, v);
+                tc::ld16x256_x4(tb + (16u << 16) + c * 32, v + 16);
+                tc::wait_ld();
+                if (PARTIALS) partials(v, 4, c * 4);
+                else promote(v, 4, c * 4);
+            }
+            {  // block 8
+                uint32_t v[8];
+                tc::ld16x256_x1(tb + 64, v);
+                tc::ld16x256_x1(tb + (16u << 16) + 64, v + 4);
+                tc::wait_ld();
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[b]);
+                if (PARTIALS) partials(v, 1, 8);
+                else promote(v, 1, 8);
             }
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            if (++s == S) s = 0;
         }
         if constexpr (!PARTIALS) {
-            if (r < nsub * 16) {
-                const int n = tile * 128 + r;
-#pragma unroll 4
-                for (int c = 0; c < NC; ++c) {
-                    const int m = tt * PT + h * NC + c;
-                    if (m >= a.M) break;
-                    const bool is16 = token_bits(a, m) == 16;
-                    if (is16 != (MODE == PMODE_BF16)) continue;
-                    const size_t o = (size_t)m * L.N + n;
-                    if (a.y_dtype == 0)
-                        reinterpret_cast<float*>(a.y)[o] = facc[c];
-                    else
-                        reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(facc[c]);
-                }
+            // Epilogue: transpose the 128 x 144 tile through (now idle) stage
+            // memory ([column][row], row stride padded by 16 B against bank
+            // conflicts), then write each token's row segment with 16-B stores.
+            ptx::named_bar_sync(1, 256);  // all promotion warps are past their last stage read
+            const int es = a.y_dtype == 0 ? 4 : 2;
+            const int rowp = 128 * es + 16;
+#pragma unroll
+            for (int i = 0; i < NB * 8; ++i) {
+                const int blk = i >> 3, si = (i >> 2) & 1, j = i & 3;
+                const int r = 32 * q + 16 * si + gid + 8 * (j >> 1);
+                const int c = h * NC + blk * 8 + 2 * t + (j & 1);
+                uint8_t* o = stage0 + c * rowp + r * es;
+                if (es == 4)
+                    *reinterpret_cast<float*>(o) = facc[i];
+                else
+                    *reinterpret_cast<__nv_bfloat16*>(o) = __float2bfloat16_rn(facc[i]);
+            }
+            ptx::named_bar_sync(1, 256);
+            const int cpc = 128 * es / 16;  // 16-B chunks per token column
+            const int valid = nsub * 16 * es / 16;
+            for (int k = threadIdx.x - PR_WARP0 * 32; k < PT * cpc; k += 256) {
+                const int c = k / cpc, part = k - c * cpc;
+                if (part >= valid || s_col[c] == 0) continue;
+                const size_t m = (size_t)tt * PT + c;
+                const uint4 v = *reinterpret_cast<const uint4*>(stage0 + c * rowp + part * 16);
+                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.y) + (m * L.N + tile * 128) * es + part * 16) = v;
             }
         }
     }
@@ -369,11 +383,12 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 }
 
 // -------------------------------------------- prefill activation quantizer
-// One warp per (token tile tt, operand row 0..PTE-1, group g).  Rows < 144 are
-// tokens: integer rows get Eq. (2) codes -- centred (Xq - z_x, s8) when the tile
-// runs in INTC mode, raw u8 otherwise -- and their scales; A16 rows get a bf16
-// copy for the bypass path; padding rows are zero.  Row 144 is the all-ones
-// column (INTU mode), rows 145.. are zero.
+// One warp per (token tile tt, token row 0..143, group g).  Writes the B operand
+// in the UMMA canonical K-major bf16 layout
+//   [tt][g][K step ks][row>>3][kk>>3][row&7][kk&7]   (16 k per K step)
+// holding the centred codes Xq - z_x of Eq. (2) for integer tokens (exact in
+// bf16), x itself for A16 tokens and 0 for absent rows; and s_x per token
+// (1 for A16 tokens, 0 for absent rows).
 __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
                                     const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ act,
                                     PreActLayout P, int64_t* err) {
@@ -381,29 +396,11 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
     const int lane = threadIdx.x & 31;
     const int NG = L.NG, G = L.G;
     const int TT = (M + PT - 1) / PT;
-    if (wid >= TT * PTE * NG) return;
+    if (wid >= TT * PT * NG) return;
     const int g = wid % NG;
-    const int row = (wid / NG) % PTE;
-    const int tt = wid / (NG * PTE);
+    const int row = (wid / NG) % PT;
+    const int tt = wid / (NG * PT);
     const size_t tg = (size_t)tt * NG + g;
-    uint8_t* cg = act + P.codes_off + tg * P.codes_group;
-    auto code_at = [&](int k) -> uint8_t* {
-        const int ks = k >> 5, kb = k & 31;
-        return cg + ks * (PTE * 32) + (row >> 3) * 256 + (kb >> 4) * 128 + (row & 7) * 16 + (kb & 15);
-    };
-    // tile mode (identical rule in the GEMM kernel): centred iff W4 and no A8 token
-    int fl = 0;
-    for (int i = lane; i < PT; i += 32) {
-        const int mm = tt * PT + i;
-        if (mm < M) fl |= tile_flags_from_bits(row_bits ? row_bits[mm] : bits);
-    }
-    fl = __reduce_or_sync(0xffffffffu, fl);
-    const bool centred = (L.wbits == 4) && !(fl & 4);
-    if (row >= PT) {  // ones column (uncentred tiles) / padding
-        const uint8_t val = (row == PT && !centred) ? 1 : 0;
-        for (int k = lane; k < G; k += 32) *code_at(k) = val;
-        return;
-    }
     const int m = tt * PT + row;
     const int b = m < M ? (row_bits ? row_bits[m] : bits) : 0;
     uint8_t* xg = act + P.x16_off + tg * P.x16_group;
@@ -413,7 +410,6 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
                                            (kk & 7) * 2);
     };
     float* sxo = reinterpret_cast<float*>(act + P.par_off + tg * PAR_BYTES) + row;
-    uint32_t* cxo = reinterpret_cast<uint32_t*>(act + P.par_off + tg * PAR_BYTES + PT * 4) + row;
     const uint16_t* src = x + (size_t)m * L.K + (size_t)g * G;
     constexpr int MAXV = 4;
     float v[MAXV];
@@ -440,15 +436,9 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
 #pragma unroll
         for (int i = 0; i < MAXV; ++i) {
             const int k = lane + 32 * i;
-            if (k < G) {
-                *code_at(k) = 0;
-                *x16_at(k) = (b == 16) ? raw[i] : (uint16_t)0;
-            }
+            if (k < G) *x16_at(k) = (b == 16) ? raw[i] : (uint16_t)0;
         }
-        if (lane == 0) {
-            *sxo = 0.f;
-            *cxo = 0u;
-        }
+        if (lane == 0) *sxo = b == 16 ? 1.f : 0.f;
         return;
     }
     vmin = warp_min(vmin);
@@ -456,33 +446,26 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
     float s;
     int z;
     fit_params(vmin, vmax, b, &s, &z);
-    int sum = 0;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
         const int k = lane + 32 * i;
         if (k < G) {
             const int qv = quantize_one(v[i], s, z, b, L.round_mode);
-            sum += qv;
-            *code_at(k) = centred ? (uint8_t)(int8_t)(qv - z) : (uint8_t)qv;
-            *x16_at(k) = 0;
+            *x16_at(k) = __bfloat16_as_ushort(__float2bfloat16_rn((float)(qv - z)));  // |qv - z| <= 255: exact
         }
     }
-    sum = warp_sum_i(sum);
-    if (lane == 0) {
-        *sxo = s;
-        *cxo = ((uint32_t)z << 16) | (uint32_t)sum;
-    }
+    if (lane == 0) *sxo = s;
 }
 
 // ------------------------------------------------------------------ host
 PreActLayout pre_act_layout(const WLayout& L, int M) {
     PreActLayout P;
     const int TT = (M + PT - 1) / PT;
-    P.codes_group = (size_t)(L.G / 32) * PTE * 32;
-    P.x16_group = (size_t)(L.G / 16) * PT * 32;
+    P.codes_group = 0;
     P.codes_off = 0;
-    P.x16_off = ((size_t)TT * L.NG * P.codes_group + 255) & ~(size_t)255;
-    P.par_off = P.x16_off + (((size_t)TT * L.NG * P.x16_group + 255) & ~(size_t)255);
+    P.x16_group = (size_t)(L.G / 16) * PT * 32;
+    P.x16_off = 0;
+    P.par_off = ((size_t)TT * L.NG * P.x16_group + 255) & ~(size_t)255;
     P.bytes = P.par_off + (((size_t)TT * L.NG * PAR_BYTES + 255) & ~(size_t)255);
     return P;
 }
@@ -491,30 +474,28 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
                                  void* act, int64_t* err, cudaStream_t st) {
     const PreActLayout P = pre_act_layout(L, M);
     const int TT = (M + PT - 1) / PT;
-    const long long warps = (long long)TT * PTE * L.NG;
+    const long long warps = (long long)TT * PT * L.NG;
     actquant_pre_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
         L, x, M, row_bits, bits, reinterpret_cast<uint8_t*>(act), P, err);
     return check_launch("actquant_pre_kernel");
 }
 
-template <int WBITS, int SPG, int MODE, bool PARTIALS>
+template <int WBITS, int SPG, bool PARTIALS>
 static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
     PreArgs a = a0;
     constexpr int G = SPG * 64;
-    constexpr bool INT = MODE != PMODE_BF16;
     const int raw = SPG * 8 * 512 * (WBITS / 4);
-    const int bbytes = INT ? (G / 32) * PTE * 32 : (G / 16) * PT * 32;
-    const int abytes = INT ? (G / 32) * 4096 : (G / 16) * 4096;
+    const int bbytes = (G / 16) * PT * 32;
     a.off_meta = raw;
     a.off_b = (a.off_meta + META_BLOCK + 127) & ~127;
     a.off_par = a.off_b + bbytes;
-    a.off_a = (a.off_par + PAR_BYTES + 127) & ~127;
-    a.stage_bytes = (a.off_a + abytes + 127) & ~127;
-    a.stages = (200 * 1024) / a.stage_bytes;
+    a.off_a = 0;  // the A operand lives in TMEM
+    a.stage_bytes = (a.off_par + PAR_BYTES + 127) & ~127;
+    a.stages = (220 * 1024) / a.stage_bytes;
     if (a.stages > 8) a.stages = 8;
     if (a.stages < 2) a.stages = 2;
     const size_t smem = 1024 + (size_t)a.stages * a.stage_bytes;
-    auto kern = qlinear_prefill_kernel<WBITS, SPG, MODE, PARTIALS>;
+    auto kern = qlinear_prefill_kernel<WBITS, SPG, PARTIALS>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -524,12 +505,11 @@ static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int MODE, bool PARTIALS>
+template <bool PARTIALS>
 static cudaError_t pre_dispatch(const PreArgs& a, dim3 grid, cudaStream_t st) {
     if (a.L.wbits == 4)
-        return a.L.G == 64 ? pre_launch<4, 1, MODE, PARTIALS>(a, grid, st) : pre_launch<4, 2, MODE, PARTIALS>(a, grid, st);
-    if (MODE == PMODE_INTC) return cudaSuccess;  // W8 codes never fit the centred s8 operand
-    return a.L.G == 64 ? pre_launch<8, 1, MODE, PARTIALS>(a, grid, st) : pre_launch<8, 2, MODE, PARTIALS>(a, grid, st);
+        return a.L.G == 64 ? pre_launch<4, 1, PARTIALS>(a, grid, st) : pre_launch<4, 2, PARTIALS>(a, grid, st);
+    return a.L.G == 64 ? pre_launch<8, 1, PARTIALS>(a, grid, st) : pre_launch<8, 2, PARTIALS>(a, grid, st);
 }
 
 dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,
@@ -547,16 +527,7 @@ dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* met
     a.act = reinterpret_cast<const uint8_t*>(act);
     a.P = pre_act_layout(L, M);
     const dim3 grid(L.T128, (M + PT - 1) / PT);
-    // three kernel variants; each CTA runs only if its token tile needs it
-    cudaError_t e;
-    if (I_out) {
-        e = pre_dispatch<PMODE_INTC, true>(a, grid, st);
-        if (e == cudaSuccess) e = pre_dispatch<PMODE_INTU, true>(a, grid, st);
-    } else {
-        e = pre_dispatch<PMODE_INTC, false>(a, grid, st);
-        if (e == cudaSuccess) e = pre_dispatch<PMODE_INTU, false>(a, grid, st);
-        if (e == cudaSuccess) e = pre_dispatch<PMODE_BF16, false>(a, grid, st);
-    }
+    const cudaError_t e = I_out ? pre_dispatch<true>(a, grid, st) : pre_dispatch<false>(a, grid, st);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "qlinear_prefill_kernel launch: %s", cudaGetErrorString(e));
     return DYQ_OK;
 }

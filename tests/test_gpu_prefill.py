@@ -111,3 +111,38 @@ def test_prefill_matches_decode_path():
         finally:
             dyq.set_path(0)
     assert np.array_equal(out[0], out[1])
+
+
+def _extreme(rows, K, G, rng):
+    """Every (row, group) constant +-c: the zero-inclusive fit puts every code at
+    an end of the range, so |q - z| = 2^b - 1 for every element."""
+    sign = rng.choice([-1.0, 1.0], size=(rows, K // G))
+    mag = rng.uniform(0.5, 2.0, size=(rows, K // G))
+    v = np.repeat(sign * mag, G, axis=1)
+    return synth.f32_to_bf16_bits(v.astype(np.float32))
+
+
+@pytest.mark.parametrize("wbits", [4, 8])
+@pytest.mark.parametrize("abits", [2, 4, 8, "mixed"])
+@pytest.mark.parametrize("G", [64, 128])
+def test_prefill_extreme_codes_exact(wbits, abits, G):
+    """Largest group sums the method can produce (|I| = G (2^bw - 1)(2^ba - 1),
+    8.3e6 for W8 A8 G128) come back bit-exact from the fp32 tensor-core
+    accumulator."""
+    M, N, K = 160, 256, 512
+    rng = np.random.default_rng(wbits * 7 + G + (0 if abits == "mixed" else abits))
+    w = _extreme(N, K, G, rng)
+    x = _extreme(M, K, G, rng)
+    rb = _rb(M, abits)
+    pk = oracle.pack_weights(w, G, wbits)
+    yref, Iref = oracle.qlinear(x, pk, G, rb, want_I=True)
+    if abits in (8, "mixed") and wbits == 8:
+        assert np.abs(Iref).max() == G * 255 * 255
+    wd, codes, meta = gpu_pack(w, G, wbits)
+    ws = _ws(wd, M)
+    I = torch.full((M, N, K // G), -7, dtype=torch.int32, device=DEV)
+    dyq.qlinear_i32_partials(wd, codes, meta, t_u16(x), M, torch.from_numpy(rb).to(DEV), 0, I, ws)
+    assert np.array_equal(I.cpu().numpy(), Iref)
+    y = torch.zeros(M, N, dtype=torch.float32, device=DEV)
+    dyq.qlinear(wd, codes, meta, t_u16(x), M, torch.from_numpy(rb).to(DEV), 0, y, 0, ws)
+    check_close(y.cpu().numpy(), yref, 1e-3)
