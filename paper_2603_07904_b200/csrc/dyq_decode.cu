@@ -53,7 +53,7 @@ struct DecArgs {
     int gps;                // groups (units) per stage
     int stages, stage_bytes;
     int off_meta, off_par, off_xq, off_x16;  // offsets inside a stage
-    int debug_skip;         // DYQ_DEBUG_SKIP=1: consumers skip the math (copy-path timing only)
+    int debug_skip;         // DYQ_DEBUG_SKIP=1: consumers skip the math (copy-path timing only; debug)
 };
 
 __device__ __forceinline__ void mma_u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -110,7 +110,7 @@ __device__ __forceinline__ uint32_t u8pair_to_bf16(uint32_t v, int hi_pair, uint
     }
 }
 
-constexpr int DEC_CWARPS = 16;  // consumer warps: 2 per 16-row sub-tile (alternate groups)
+constexpr int DEC_CWARPS = 16;  // consumer warps: (sub-tile w & 7) x (stage parity w >> 3)
 constexpr int DEC_THREADS = 32 * (DEC_CWARPS + 1);  // + 1 producer warp
 constexpr int DEC_CONSUMERS = 32 * DEC_CWARPS;
 
@@ -154,15 +154,13 @@ __device__ __forceinline__ void dec_flush(const DecArgs& a, int tile, const floa
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int tok = j * 8 + 2 * t + (i & 1);
-                __stcg(&P[tok * 128 + warp * 16 + gid + 8 * (i >> 1)], facc[j][i]);
+                P[tok * 128 + warp * 16 + gid + 8 * (i >> 1)] = facc[j][i];
             }
     }
-    __threadfence();
     ptx::named_bar_sync(1, DEC_CONSUMERS);
-    if (threadIdx.x == 0) *s_flag = (atomicAdd(&a.counters[tile], 1) == nc - 1);
+    if (threadIdx.x == 0) *s_flag = (ptx::atom_add_acq_rel_gpu(&a.counters[tile], 1) == nc - 1);
     ptx::named_bar_sync(1, DEC_CONSUMERS);
     if (*s_flag) {
-        __threadfence();
         for (int idx = threadIdx.x; idx < a.M * nrows; idx += DEC_CONSUMERS) {
             const int tok = idx / nrows, r = idx - tok * nrows;
             // all slot loads in flight before the (slot-ordered, deterministic) sum
@@ -323,20 +321,20 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
 }
 
 // Consumer loop over the CTA's stages (must enumerate stages exactly like the
-// producer).  Consumer warp w works on sub-tile w & 7 and on every other group
-// of each stage (half = w >> 3); the two halves are combined through shared
-// memory before a tile is flushed.
+// producer).  Consumer warp w works on sub-tile w & 7 for every group of the
+// stages of parity w >> 3; the two parities' partial sums are combined through
+// shared memory only when a tile is flushed.
 template <int NT8>
-__device__ __forceinline__ void combine_halves(float (&facc)[NT8][4], float* scr, int half, int sub, int lane) {
+__device__ __forceinline__ void combine_parities(float (&facc)[NT8][4], float* scr, int par, int sub, int lane) {
     float* p = scr + (sub * 32 + lane) * (NT8 * 4);
-    if (half == 1) {
+    if (par == 1) {
 #pragma unroll
         for (int j = 0; j < NT8; ++j)
 #pragma unroll
             for (int k = 0; k < 4; ++k) p[j * 4 + k] = facc[j][k];
     }
     ptx::named_bar_sync(2, DEC_CONSUMERS);
-    if (half == 0) {
+    if (par == 0) {
 #pragma unroll
         for (int j = 0; j < NT8; ++j)
 #pragma unroll
@@ -353,10 +351,10 @@ __device__ __forceinline__ void dec_consume(const DecArgs& a, uint32_t bar_full,
     const int NG = L.NG;
     const int S = a.stages;
     const int lane = threadIdx.x & 31, cw = threadIdx.x >> 5;
-    const int sub = cw & 7, half = cw >> 3;
+    const int sub = cw & 7, par = cw >> 3;
     const int gid = lane >> 2, t = lane & 3;
     const uint32_t stage_bytes = (uint32_t)a.stage_bytes;
-    int s = 0;
+    int s = 0, i = 0;
     uint32_t ph = 0;
     int cur_tile = -1;
     float facc[NT8][4];
@@ -366,15 +364,15 @@ __device__ __forceinline__ void dec_consume(const DecArgs& a, uint32_t bar_full,
         for (int k = 0; k < 4; ++k) facc[j][k] = 0.f;
     const int gps = a.gps;
     int tile = u0 / NG, g0 = u0 - (u0 / NG) * NG;  // one division per CTA, then incremental
-    for (int u = u0; u < u1;) {
+    for (int u = u0; u < u1; ++i) {
         if (g0 == NG) { g0 = 0; ++tile; }
         int n = NG - g0;
         n = n < gps ? n : gps;
         n = n < u1 - u ? n : u1 - u;
         if (!PARTIALS && tile != cur_tile) {
             if (cur_tile >= 0) {
-                combine_halves<NT8>(facc, scr, half, sub, lane);
-                dec_flush<NT8>(a, cur_tile, facc, half ? 8 : sub, gid, t, s_flag);
+                combine_parities<NT8>(facc, scr, par, sub, lane);
+                dec_flush<NT8>(a, cur_tile, facc, par ? 8 : sub, gid, t, s_flag);
             }
             cur_tile = tile;
 #pragma unroll
@@ -382,23 +380,26 @@ __device__ __forceinline__ void dec_consume(const DecArgs& a, uint32_t bar_full,
 #pragma unroll
                 for (int k = 0; k < 4; ++k) facc[j][k] = 0.f;
         }
-        const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
-        ptx::mbar_wait_u32(bar_full + 8 * s, ph);
-        if (sub < nsub && !a.debug_skip) {
-            const uint32_t st = stage0 + s * stage_bytes;
-            for (int gi = half; gi < n; gi += 2)
-                dec_group<WBITS, NT8, SPG, MODE, PARTIALS>(a, st, gi, g0 + gi, tile, nsub, facc, is16_mask);
+        if ((i & 1) == par) {
+            const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
+            ptx::mbar_wait_u32(bar_full + 8 * s, ph);
+            if (sub < nsub && a.debug_skip == 0) {
+                const uint32_t st = stage0 + s * stage_bytes;
+#pragma unroll 2
+                for (int gi = 0; gi < n; ++gi)
+                    dec_group<WBITS, NT8, SPG, MODE, PARTIALS>(a, st, gi, g0 + gi, tile, nsub, facc, is16_mask);
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_u32(bar_empty + 8 * s);
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_u32(bar_empty + 8 * s);
         if (++s == S) { s = 0; ph ^= 1; }
         u += n;
         g0 += n;
     }
     if constexpr (!PARTIALS) {
         if (cur_tile >= 0) {
-            combine_halves<NT8>(facc, scr, half, sub, lane);
-            dec_flush<NT8>(a, cur_tile, facc, half ? 8 : sub, gid, t, s_flag);
+            combine_parities<NT8>(facc, scr, par, sub, lane);
+            dec_flush<NT8>(a, cur_tile, facc, par ? 8 : sub, gid, t, s_flag);
         }
     }
 }
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(DEC_THREADS) qlinear_decode_kernel(const DecAr
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], DEC_CWARPS);
+            ptx::mbar_init(&empty[s], DEC_CWARPS / 2);  // the 8 warps of the stage's parity
         }
         ptx::fence_mbar_init();
     }
@@ -577,7 +578,7 @@ static DecPlan dec_plan(const WLayout& L, int nt8) {
     p.stages = (smem_kb * 1024 - 256) / p.stage_bytes;
     p.stages = p.stages < 2 ? 2 : (p.stages > 32 ? 32 : p.stages);
     p.smem = 128 * ((16 * p.stages + 4 + 127) / 128) + (size_t)p.stages * p.stage_bytes +
-             (size_t)8 * 32 * 8 * 4;  // + half-combine scratch
+             (size_t)8 * 32 * 8 * 4;  // + parity-combine scratch
     const int U = L.T128 * L.NG;
     static const int ctas = env_int("DYQ_DEC_CTAS", 1);
     const int target = num_sms() * ctas;
