@@ -285,7 +285,7 @@ def main():
 
     bytes_step = sum(algo_bytes(N, K, M, G, WB) for _, N, K in lins)
     gate_li = [n for n, _, _ in lins].index("gate_up")
-    n_launch_step = 2 + len(lins)
+    n_launch_step = 2 + 2 * len(lins)  # select_bits, route_bits, then act-quant + qlinear kernel per linear
 
     def step(t, fixed_bits=None, ev=None):
         c = t % C

@@ -11,11 +11,12 @@
 //    consecutive units of one tile (~16 KB of codes: one bulk copy) + their
 //    metadata (one copy) + the activation slices (one copy per array) -- big
 //    copies keep the TMA engine's per-copy cost off the critical path;
-//  * one CTA per SM (stream-K: contiguous unit ranges, tile-major), sized to
-//    ~half the shared memory so the NEXT kernel's CTA co-resides and starts
-//    streaming its weights under programmatic dependent launch (PDL);
+//  * one CTA per SM (stream-K: contiguous unit ranges, tile-major); the
+//    producer issues the first stages' WEIGHT copies before griddepcontrol.wait,
+//    so weight streaming starts under programmatic dependent launch (PDL);
 //  * one producer thread runs an S-stage mbarrier ring (cp.async.bulk);
-//  * 8 consumer warps, warp w = 16-row sub-tile w: one LDS.128 per lane is the
+//  * 16 consumer warps, warp w = 16-row sub-tile w & 7, working on every group
+//    of the stages of parity w >> 3: one LDS.128 per lane is the
 //    exact register image of two mma.m16n8k32 A fragments (pre-permuted by
 //    dyq_pack_weights); nibbles widen with LOP3s; integer tokens run
 //    IMMA.16832.U8.U8 (tokens = the n8 dimension) with the exact per-group

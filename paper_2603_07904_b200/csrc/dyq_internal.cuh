@@ -77,11 +77,12 @@ __host__ __device__ inline size_t act_xq_index(int NG, int G, int m, int g, int 
     return (((size_t)(m >> 3) * NG + g) * 8 + (m & 7)) * G + pos;
 }
 
-// Prefill activation operand (M > 16): per (128-token tile, K-group) the
-// UMMA canonical K-major no-swizzle blocks the tcgen05 kernel bulk-copies:
-//   codes [TT][NG][G/32 K-steps][144 rows][32 B]  (row 128 = all-ones column)
-//   x16   [TT][NG][G/16 K-steps][128 rows][16 bf16] (A16 rows, else 0)
-//   par   [TT][NG][128] {float s_x; uint32 (z_x << 16) | SX}
+// Prefill activation operand (M > 16): per (144-token tile, K-group) the UMMA
+// canonical K-major no-swizzle B operand of the tcgen05 kernel,
+//   x16 [TT][NG][G/16 K-steps][144 rows] bf16: centred codes Xq - z_x (exact),
+//       x for A16 rows, 0 for absent rows
+//   par [TT][NG][144] f32 s_x (1 for A16 rows, 0 for absent rows)
+// (codes_off / codes_group are unused, kept 0).
 struct PreActLayout {
     size_t codes_off, x16_off, par_off, bytes;
     size_t codes_group, x16_group;
