@@ -60,6 +60,7 @@ def parse():
     p.add_argument("--trials", type=int, default=5, help="timed repetitions of the K-step region")
     p.add_argument("--no-variants", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-prefill", action="store_true", help="skip the configs[2] prefill slice")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu)")
     return p.parse_args()
 
@@ -239,7 +240,7 @@ def main():
     import torch.distributed as dist
 
     import synth
-    from paper_2603_07904_b200 import dyq
+    from paper_2603_07904_b200 import dyq, episodes
     from paper_2603_07904_b200 import build as _b
     _b.build()
 
@@ -272,7 +273,8 @@ def main():
 
     # ---- kinematic state and trajectory (episode seed per rank)
     T = HISTORY_STEPS + args.warmup + args.steps * (args.trials + 1) + 2
-    acts_np = synth.trajectories(1, T, seed0=2000 + rank)
+    my_eps = episodes.shard(world, world, rank)  # one episode (control stream) per rank
+    acts_np = synth.trajectories(1, T, seed0=episodes.episode_seed(my_eps[0]))
     acts = torch.from_numpy(acts_np).to(dev)
     cal = dyq.default_calib()
     state = torch.zeros(dyq.state_size(1, cal), dtype=torch.uint8, device=dev)
@@ -339,12 +341,7 @@ def main():
         g.replay()
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = float(tt.item())
-        return ms
+        return episodes.max_over_ranks(e0.elapsed_time(e1), device=dev)
 
     graph.replay()  # one untimed replay (warm graph)
     torch.cuda.synchronize()
@@ -361,7 +358,7 @@ def main():
                     events_ok = False
     ms_total = statistics.median(trial_ms)
     ms_step = ms_total / args.steps
-    value = bytes_step * world / (ms_step * 1e-3) / 1e9
+    value = episodes.throughput(bytes_step, ms_step * 1e-3) / 1e9  # all ranks' bytes / slowest rank
 
     # ---- bits histogram over the timed steps (read back once, outside timing)
     hist = {}
@@ -424,6 +421,55 @@ def main():
                 "us_per_block": round(ms * 1e3, 2)}
             del g2
 
+    # ---- configs[2] slice: prefill of one block at M = 288 tokens (256 vision +
+    # 32 text) with the step's b*, on the tcgen05 path (tensor-bound)
+    prefill = None
+    if not args.profile and not args.no_prefill:
+        MP = 288
+        xps = [synth.activations_bf16_torch(MP, K, seed=5000 + li, device=dev) for li, (_, _, K) in enumerate(lins)]
+        yps = [torch.empty(MP, N, dtype=torch.bfloat16, device=dev) for (_, N, _) in lins]
+        wps = [packed[0][li].workspace(MP) for li in range(len(lins))]
+        rbp = torch.zeros(MP, dtype=torch.int32, device=dev)
+
+        def pstep(t, fixed_bits=None):
+            if fixed_bits is None:
+                dyq.route_bits(bits, 1, MP, rbp)
+                rb, b = rbp, 0
+            else:
+                rb, b = None, fixed_bits
+            for li in range(len(lins)):
+                p = packed[t % C][li]
+                dyq.qlinear(p.wd, p.codes, p.meta, xps[li], MP, rb, b, yps[li], 1, wps[li])
+
+        ops_block = sum(2 * MP * N * K for _, N, K in lins)
+        i8_peak = 4500.0  # TOPS, nominal dense int8 (north_star: integer tensor-pipe peak)
+        bf16_peak = float((peaks() or {}).get("bf16_tflops", 2250.0))
+        pres = {}
+        for fb in (None, 2, 4, 8, 16):
+            for i in range(2):
+                pstep(i, fb)
+            torch.cuda.synchronize()
+            gp = torch.cuda.CUDAGraph()
+            sp = torch.cuda.Stream()
+            sp.wait_stream(torch.cuda.current_stream())
+            RP = 10
+            with torch.cuda.graph(gp, stream=sp):
+                for i in range(RP):
+                    pstep(i, fb)
+            gp.replay()
+            torch.cuda.synchronize()
+            ms = statistics.median(timed(gp) for _ in range(3)) / RP
+            tops = ops_block / (ms * 1e-3) / 1e12
+            pres["step_bits" if fb is None else f"W{WB}A{fb}"] = {
+                "us_per_block": round(ms * 1e3, 1), "int_TOPS": round(tops, 1),
+                "frac_i8_nominal": round(tops / i8_peak, 4), "frac_bf16_pipe": round(tops / bf16_peak, 4)}
+            del gp
+        prefill = {"workload": "configs[2] slice: one Llama-2-7B block prefill, M=288 (256 vision + 32 text), "
+                               f"W{WB} G={G}, b* of the current step; whole backbone = 32 x this",
+                   "kernel": "qlinear_prefill_kernel (tcgen05 kind::f16, exact integer operands, A in TMEM)",
+                   "peak_i8_TOPS": i8_peak, "peak_bf16_TFLOPS": bf16_peak, "results": pres,
+                   "timing": "cuda events around a graph of 10 blocks (median of 3)"}
+
     # ---- e2e through the public API: pinned H2D of the step's inputs, eager
     # launches, D2H of the step's result (block output y and b*), per step
     e2e = None
@@ -454,11 +500,7 @@ def main():
             y_host.copy_(ys[-1], non_blocking=True)
             b_host.copy_(bits, non_blocking=True)
             torch.cuda.current_stream().synchronize()
-        dt = (time.perf_counter() - tc) / n_e2e
-        if world > 1:
-            tt = torch.tensor([dt], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
+        dt = episodes.max_over_ranks((time.perf_counter() - tc) / n_e2e, device=dev)
         e2e = {"value": round(bytes_step * world / dt / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(dt * 1e3, 4), "steps": n_e2e,
@@ -482,6 +524,7 @@ def main():
             "bits_hist_timed": {str(k): v for k, v in sorted(hist.items())},
             "roofline": roofline,
             "variants": variants,
+            "prefill": prefill,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
