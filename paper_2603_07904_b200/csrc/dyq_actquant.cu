@@ -23,7 +23,9 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
     uint8_t* dq = ws + A.xq_off + xi;
     uint16_t* d16 = reinterpret_cast<uint16_t*>(ws + A.x16_off) + xi;
     uint2* pdst = reinterpret_cast<uint2*>(ws + A.par_off) + (size_t)g * DEC_MPAD + m;
+    uint8_t* zdst = ws + A.zx_off + (size_t)g * DEC_MPAD + m;
     const int b = (m < M) ? (row_bits ? row_bits[m0 + m] : bits) : 0;
+    const bool centred = dec_call_centred(M, m0, row_bits, bits);
     const uint16_t* src = x + (size_t)(m0 + m) * L.K + (size_t)g * L.G;
     constexpr int MAXV = 4;  // G <= 128
     float v[MAXV];
@@ -57,7 +59,10 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
                 d16[pos] = (b == 16) ? raw[i] : (uint16_t)0;
             }
         }
-        if (lane == 0) *pdst = make_uint2(0u, 0u);
+        if (lane == 0) {
+            *pdst = make_uint2(0u, 0u);
+            *zdst = 0;
+        }
         return;
     }
     vmin = warp_min(vmin);
@@ -73,12 +78,15 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
             const int q = quantize_one(v[i], s, z, b, L.round_mode);
             sum += q;
             const int pos = (k & ~63) + dec_perm(k & 63);
-            dq[pos] = (uint8_t)q;
+            dq[pos] = centred ? (uint8_t)(int8_t)(q - z) : (uint8_t)q;
             d16[pos] = 0;
         }
     }
     sum = warp_sum_i(sum);
-    if (lane == 0) *pdst = make_uint2(__float_as_uint(s), ((uint32_t)z << 16) | (uint32_t)sum);
+    if (lane == 0) {
+        *pdst = make_uint2(__float_as_uint(s), centred ? (uint32_t)(sum - L.G * z) : ((uint32_t)z << 16) | (uint32_t)sum);
+        *zdst = (uint8_t)z;
+    }
 }
 
 dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int m0, const int32_t* row_bits,
@@ -102,28 +110,33 @@ dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int
 }
 
 // Test hook: export the decode-layout activation codes in logical layout.
-__global__ void actquant_export_kernel(WLayout L, int M, int m0, const uint8_t* __restrict__ ws, ActLayoutDec A,
-                                       uint8_t* oq, float* os, uint8_t* oz, int32_t* oSX) {
+__global__ void actquant_export_kernel(WLayout L, int M, int m0, const int32_t* __restrict__ row_bits, int bits,
+                                       const uint8_t* __restrict__ ws, ActLayoutDec A, uint8_t* oq, float* os,
+                                       uint8_t* oz, int32_t* oSX) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)M * L.K) return;
     const int m = (int)(idx / L.K), k = (int)(idx % L.K);
     const int g = k / L.G, kk = k % L.G;
     const int pos = (kk & ~63) + dec_perm(kk & 63);
-    oq[(size_t)(m0 + m) * L.K + k] = ws[A.xq_off + act_xq_index(L.NG, L.G, m, g, pos)];
+    const bool centred = dec_call_centred(M, m0, row_bits, bits);
+    const int z = ws[A.zx_off + (size_t)g * DEC_MPAD + m];
+    const uint8_t c = ws[A.xq_off + act_xq_index(L.NG, L.G, m, g, pos)];
+    const int b = row_bits ? row_bits[m0 + m] : bits;
+    oq[(size_t)(m0 + m) * L.K + k] = (centred && b != 16) ? (uint8_t)((int)(int8_t)c + z) : c;
     if (kk == 0) {
         const uint2 p = reinterpret_cast<const uint2*>(ws + A.par_off)[(size_t)g * DEC_MPAD + m];
         os[(size_t)(m0 + m) * L.NG + g] = __uint_as_float(p.x);
-        oz[(size_t)(m0 + m) * L.NG + g] = (uint8_t)(p.y >> 16);
-        oSX[(size_t)(m0 + m) * L.NG + g] = (int32_t)(p.y & 0xffffu);
+        oz[(size_t)(m0 + m) * L.NG + g] = (uint8_t)z;
+        oSX[(size_t)(m0 + m) * L.NG + g] = centred ? (int32_t)p.y + L.G * z : (int32_t)(p.y & 0xffffu);
     }
 }
 
-dyq_status_t launch_actquant_export(const WLayout& L, int M, const void* ws, uint8_t* xq, float* sx,
-                                    uint8_t* zx, int32_t* SX, int m0, cudaStream_t st) {
+dyq_status_t launch_actquant_export(const WLayout& L, int M, const int32_t* row_bits, int bits, const void* ws,
+                                    uint8_t* xq, float* sx, uint8_t* zx, int32_t* SX, int m0, cudaStream_t st) {
     const ActLayoutDec A = act_layout_dec(L);
     const size_t total = (size_t)M * L.K;
     actquant_export_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
-        L, M, m0, reinterpret_cast<const uint8_t*>(ws), A, xq, sx, zx, SX);
+        L, M, m0, row_bits, bits, reinterpret_cast<const uint8_t*>(ws), A, xq, sx, zx, SX);
     return check_launch("actquant_export_kernel");
 }
 

@@ -65,6 +65,14 @@ __device__ __forceinline__ void mma_u8(int (&c)[4], const uint32_t (&a)[4], uint
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
 __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -115,7 +123,7 @@ constexpr int DEC_CWARPS = 16;  // consumer warps: (sub-tile w & 7) x (stage par
 constexpr int DEC_THREADS = 32 * (DEC_CWARPS + 1);  // + 1 producer warp
 constexpr int DEC_CONSUMERS = 32 * DEC_CWARPS;
 
-enum { MODE_INT = 0, MODE_A16 = 1, MODE_MIXED = 2 };
+enum { MODE_INT = 0, MODE_A16 = 1, MODE_MIXED = 2, MODE_INTC = 3 };  // INTC: centred s8 activation codes
 
 // Split-K tile flush: direct store when the CTA owns the whole tile, otherwise
 // private slot + last-arriver deterministic reduction.
@@ -238,7 +246,15 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
             A[0][0] = w0.x; A[0][1] = w0.y; A[0][2] = w0.z; A[0][3] = w0.w;
             A[1][0] = w1.x; A[1][1] = w1.y; A[1][2] = w1.z; A[1][3] = w1.w;
         }
-        if (MODE != MODE_A16) {
+        if (MODE == MODE_INTC) {
+            // centred s8 activations: P' = Sum q (Xq - z_x) directly
+#pragma unroll
+            for (int j = 0; j < NT8; ++j) {
+                const uint4 xb = ptx::lds128(st + a.off_xq + ((j * gps + gi) * 8 + gid) * G + spi * 64 + t * 16);
+                mma_u8s8(iacc[j], A[0], xb.x, xb.y);
+                mma_u8s8(iacc[j], A[1], xb.z, xb.w);
+            }
+        } else if (MODE != MODE_A16) {
             // Sum q for rows gid, gid+8 from an all-ones B (no shuffles)
             mma_u8(sq, A[0], ONES, ONES);
             mma_u8(sq, A[1], ONES, ONES);
@@ -249,7 +265,7 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
                 mma_u8(iacc[j], A[1], xb.z, xb.w);
             }
         }
-        if (MODE != MODE_INT) {
+        if (MODE == MODE_A16 || MODE == MODE_MIXED) {
 #pragma unroll
             for (int j = 0; j < NT8; ++j) {
                 const uint32_t xr = st + a.off_x16 + (((j * gps + gi) * 8 + gid) * G + spi * 64 + t * 16) * 2;
@@ -283,10 +299,18 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
         const int zx0 = (int)(pp.y >> 16), zx1 = (int)(pp.w >> 16);
         const int SX0 = (int)(pp.y & 0xffffu), SX1 = (int)(pp.w & 0xffffu);
         int I[4];
-        I[0] = iacc[j][0] - zw0 * SX0 - zx0 * T_g;
-        I[1] = iacc[j][1] - zw0 * SX1 - zx1 * T_g;
-        I[2] = iacc[j][2] - zw1 * SX0 - zx0 * T_g8;
-        I[3] = iacc[j][3] - zw1 * SX1 - zx1 * T_g8;
+        if (MODE == MODE_INTC) {  // par = {s_x, SXc = Sum (Xq - z_x)}
+            const int SXc0 = (int)pp.y, SXc1 = (int)pp.w;
+            I[0] = iacc[j][0] - zw0 * SXc0;
+            I[1] = iacc[j][1] - zw0 * SXc1;
+            I[2] = iacc[j][2] - zw1 * SXc0;
+            I[3] = iacc[j][3] - zw1 * SXc1;
+        } else {
+            I[0] = iacc[j][0] - zw0 * SX0 - zx0 * T_g;
+            I[1] = iacc[j][1] - zw0 * SX1 - zx1 * T_g;
+            I[2] = iacc[j][2] - zw1 * SX0 - zx0 * T_g8;
+            I[3] = iacc[j][3] - zw1 * SX1 - zx1 * T_g8;
+        }
         if constexpr (PARTIALS) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -298,7 +322,7 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
                     a.I_out[((size_t)(a.m0 + tc) * L.N + n) * L.NG + g] = a16 ? 0 : I[k];
                 }
             }
-        } else if (MODE == MODE_INT) {
+        } else if (MODE == MODE_INT || MODE == MODE_INTC) {
             // (I0, I1) * (sx0, sx1) * sw_row  with packed fp32x2
             float t0, t1, t2, t3;
             mul2(t0, t1, (float)I[0], (float)I[1], sx0, sx1);
@@ -529,7 +553,9 @@ __global__ void __launch_bounds__(DEC_THREADS) qlinear_decode_kernel(const DecAr
     const uint32_t bar_full = ptx::smem_u32(full), bar_empty = ptx::smem_u32(empty);
     const uint32_t st0 = ptx::smem_u32(stage0);
     float* scr = reinterpret_cast<float*>(stage0 + (size_t)S * stage_bytes);
-    if (PARTIALS || (any_int && any16))
+    if (!any16 && dec_call_centred(a.M, a.m0, a.row_bits, a.bits))
+        dec_consume<WBITS, NT8, SPG, MODE_INTC, PARTIALS>(a, bar_full, bar_empty, st0, s_flag, scr, u0, u1, is16_mask);
+    else if (PARTIALS || (any_int && any16))
         dec_consume<WBITS, NT8, SPG, MODE_MIXED, PARTIALS>(a, bar_full, bar_empty, st0, s_flag, scr, u0, u1, is16_mask);
     else if (any16)
         dec_consume<WBITS, NT8, SPG, MODE_A16, PARTIALS>(a, bar_full, bar_empty, st0, s_flag, scr, u0, u1, is16_mask);
@@ -590,25 +616,9 @@ static DecPlan dec_plan(const WLayout& L, int nt8) {
 }
 
 // split-K slot storage: (grid + T128) slots of 16 x 128 floats, then T128 counters
-size_t decode_ldg_ws_bytes(const WLayout& L);
-dyq_status_t launch_decode_ldg(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int M,
-                               int m0, const int32_t* row_bits, int bits, void* y, int y_dtype, int32_t* I_out,
-                               void* ws_dec, const void* act, cudaStream_t st);
-
 size_t decode_ws_bytes(const WLayout& L) {
     const DecPlan p = dec_plan(L, 2);
-    const size_t tma = (size_t)(p.grid + L.T128) * 16 * 128 * 4 + (((size_t)L.T128 * 4 + 255) & ~(size_t)255);
-    const size_t ldg = decode_ldg_ws_bytes(L);
-    return tma > ldg ? tma : ldg;
-}
-
-// DYQ_DECODE_IMPL=ldg selects the register-streaming kernel; default: bulk-copy ring
-static bool use_ldg() {
-    static const int v = [] {
-        const char* e = getenv("DYQ_DECODE_IMPL");
-        return (e && e[0] == 'l') ? 1 : 0;
-    }();
-    return v != 0;
+    return (size_t)(p.grid + L.T128) * 16 * 128 * 4 + (((size_t)L.T128 * 4 + 255) & ~(size_t)255);
 }
 
 template <int WBITS, int NT8, int SPG, bool PARTIALS>
@@ -642,9 +652,6 @@ static cudaError_t launch_k(const DecArgs& a, const DecPlan& p, cudaStream_t st)
 dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int M,
                            int m0, const int32_t* row_bits, int bits, void* y, int y_dtype, int32_t* I_out,
                            void* ws, int64_t* /*err*/, cudaStream_t st) {
-    if (use_ldg())
-        return launch_decode_ldg(L, codes, meta, x, M, m0, row_bits, bits, y, y_dtype, I_out, ws,
-                                 reinterpret_cast<uint8_t*>(ws) + ((decode_ws_bytes(L) + 255) & ~(size_t)255), st);
     const int nt8 = M <= 8 ? 1 : 2;
     const ActLayoutDec A = act_layout_dec(L);
     const DecPlan p = dec_plan(L, nt8);

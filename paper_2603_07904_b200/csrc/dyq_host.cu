@@ -56,7 +56,8 @@ ActLayoutDec act_layout_dec(const WLayout& L) {
     A.par_off = 0;
     A.xq_off = ((size_t)L.NG * DEC_MPAD * 8 + 255) & ~(size_t)255;
     A.x16_off = A.xq_off + (((size_t)DEC_MPAD * L.K + 255) & ~(size_t)255);
-    A.bytes = A.x16_off + (((size_t)DEC_MPAD * L.K * 2 + 255) & ~(size_t)255);
+    A.zx_off = A.x16_off + (((size_t)DEC_MPAD * L.K * 2 + 255) & ~(size_t)255);
+    A.bytes = A.zx_off + (((size_t)L.NG * DEC_MPAD + 255) & ~(size_t)255);
     return A;
 }
 
@@ -336,7 +337,7 @@ dyq_status_t dyq_act_quant_for_check(const dyq_wdesc_t* wd, const uint16_t* x, i
         const int mt = (M - m0) < DEC_MPAD ? (M - m0) : DEC_MPAD;
         rc = launch_actquant_dec(L, x, mt, m0, row_bits, bits, area, err, st);
         if (rc) return rc;
-        rc = launch_actquant_export(L, mt, area, xq, sx, zx, SX, m0, st);
+        rc = launch_actquant_export(L, mt, row_bits, bits, area, xq, sx, zx, SX, m0, st);
         if (rc) return rc;
     }
     return DYQ_OK;

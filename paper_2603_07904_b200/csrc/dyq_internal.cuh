@@ -70,8 +70,20 @@ __host__ __device__ inline int dec_perm(int kk) {  // kk in [0,64) -> position
 }
 
 struct ActLayoutDec {
-    size_t par_off, xq_off, x16_off, bytes;
+    size_t par_off, xq_off, x16_off, zx_off, bytes;
 };
+// Decode activation format of a call: CENTRED when every token of the call runs
+// at 2 or 4 bits -- codes stored as s8 (Xq - z_x) and par = {s_x, SXc = Sum (Xq - z_x)},
+// so the kernel needs one u8 x s8 IMMA and I = P' - z_w * SXc; otherwise RAW u8
+// codes with par = {s_x, z_x << 16 | SX}.  z_x is also kept in zx[NG][16] (test hook).
+__device__ __forceinline__ bool dec_call_centred(int M, int m0, const int32_t* row_bits, int bits) {
+    bool c = true;
+    for (int m = 0; m < M; ++m) {
+        const int b = row_bits ? row_bits[m0 + m] : bits;
+        c &= (b == 2 || b == 4);
+    }
+    return c;
+}
 // element offsets of token m, group g, in-group position pos
 __host__ __device__ inline size_t act_xq_index(int NG, int G, int m, int g, int pos) {
     return (((size_t)(m >> 3) * NG + g) * 8 + (m & 7)) * G + pos;
@@ -196,8 +208,8 @@ dyq_status_t launch_unpack(const WLayout& L, const void* codes, const void* meta
                            float* s, uint8_t* z, cudaStream_t st);
 dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int m0, const int32_t* row_bits,
                                  int bits, void* ws, int64_t* err, cudaStream_t st);
-dyq_status_t launch_actquant_export(const WLayout& L, int M, const void* ws, uint8_t* xq, float* sx,
-                                    uint8_t* zx, int32_t* SX, int m0, cudaStream_t st);
+dyq_status_t launch_actquant_export(const WLayout& L, int M, const int32_t* row_bits, int bits, const void* ws,
+                                    uint8_t* xq, float* sx, uint8_t* zx, int32_t* SX, int m0, cudaStream_t st);
 // rows m0 .. m0+M-1 (M <= DEC_MPAD); x, row_bits, y, I_out are base pointers;
 // ws = zero-initialised split-K accumulator area (decode_ws_bytes)
 dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int M,
