@@ -155,7 +155,11 @@ DYQ_API dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t toke
 /* -------------------------------------------------- activation quantizer */
 /* Workspace bytes for dyq_qlinear with M tokens against descriptor wd (holds
  * the quantized activations, their per-group parameters and the split-K
- * partials).  Must be zeroed once before first use (dyq_workspace_init). */
+ * partials).  Must be zeroed once before first use (dyq_workspace_init).  A
+ * workspace belongs to one weight SHAPE (N, K, group, wbits): it may be reused
+ * for every M and every layer of that shape (its split-K tile counters reset
+ * themselves), but not shared with another shape, whose layout would overwrite
+ * the counters. */
 DYQ_API dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* bytes);
 DYQ_API dyq_status_t dyq_workspace_init(void* workspace, size_t bytes, dyq_stream_t stream);
 
@@ -214,6 +218,75 @@ DYQ_API dyq_status_t dyq_act_quant_for_check(const dyq_wdesc_t* wd, const uint16
 /* Force the kernel family (testing / benchmarking): 0 = auto (default),
  * 1 = decode (M <= 64 only), 2 = prefill.  Process-wide. */
 DYQ_API dyq_status_t dyq_set_path(int32_t path);
+
+/* ============================================================ policy step
+ * one VLA control step around the quantized linears.  The
+ * backbone is OpenVLA's Llama-2: n_vis vision embeddings (synthetic
+ * in this repo; the vision encoder is out of scope) + n_text text tokens are
+ * prefilled through n_layers blocks
+ *   x = RMSNorm(h); qkv = qlinear(x); RoPE(q, k); a = causal attention (KV cache);
+ *   h += qlinear_o(a); x = RMSNorm(h); h += qlinear_down(SiLU(g) * u),
+ *   [g | u] = qlinear_gate_up(x)
+ * then the action head (the LM-head rows of the n_bins action-bin tokens, the
+ * last n_bins ids of the vocabulary) + argmax gives the first action token,
+ * and n_act - 1 decode passes give the rest (one b* for all tokens of the step,
+ * P:346); action value of bin b = -1 + (2b + 1) / n_bins.  Every
+ * qlinear runs at the activation bits of the episode's b*_t from
+ * dyq_select_bits through the W4-pinned variant table.
+ * All buffers are caller-owned (sizes from dyq_model_size); dyq_model_bind
+ * makes a host-side handle only (no device allocation). */
+typedef struct {
+    int32_t n_layers, d, ffn, n_heads, vocab, E; /* E = max episodes per step          */
+    int32_t n_vis, n_text, n_act, n_bins;        /* 256, 32, 7, 256 (OpenVLA)           */
+    int32_t group, wbits;                        /* packing of every linear             */
+    float rms_eps, rope_theta;                   /* 1e-5 (Llama-2: 1e-5), 10000         */
+    const void* const* codes;   /* host array [n_layers * 4] of device pointers: qkv, o, gate_up, down */
+    const void* const* meta;    /* same order                                           */
+    const uint16_t* attn_norm;  /* device bf16 [n_layers, d]                            */
+    const uint16_t* mlp_norm;   /* device bf16 [n_layers, d]                            */
+    const uint16_t* final_norm; /* device bf16 [d]                                      */
+    const uint16_t* embed;      /* device bf16 [vocab, d]                               */
+    const uint16_t* head_bins;  /* device bf16 [n_bins, d]: LM-head rows of the bin tokens */
+    void* kv;                   /* device, kv_bytes: [E][n_layers][2][T][d] bf16, T = n_vis+n_text+n_act */
+    void* scratch;              /* device, scratch_bytes (activations, qlinear workspace, ...)  */
+} dyq_model_desc_t;
+DYQ_API dyq_status_t dyq_model_size(const dyq_model_desc_t* desc, size_t* kv_bytes, size_t* scratch_bytes);
+DYQ_API dyq_status_t dyq_model_bind(const dyq_model_desc_t* desc, void** model);
+/* zero the scratch (split-K counters) and start new episodes (no prev action) */
+DYQ_API dyq_status_t dyq_model_init(void* model, dyq_stream_t stream);
+DYQ_API dyq_status_t dyq_model_free(void* model);
+/* vis_emb device bf16 [E, n_vis, d]; text_ids device int32 [E, n_text];
+ * action_out device f32 [E, n_act]; bits_out device int32 [E] (b*_t) or NULL.
+ * state = dyq_select_bits state for >= E streams.  E <= desc.E. */
+DYQ_API dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t* vis_emb,
+                                     const int32_t* text_ids, float* action_out, int32_t* bits_out,
+                                     dyq_stream_t stream);
+
+/* Glue kernels of the policy step, exported for tests (device pointers, bf16 = uint16).
+ * h (+)= delta (if delta != NULL, h updated in place); y = RMSNorm(h) * w, rows of d. */
+DYQ_API dyq_status_t dyq_add_rmsnorm(uint16_t* h, const uint16_t* delta, const uint16_t* w, int32_t M,
+                                     int32_t d, float eps, uint16_t* y, dyq_stream_t stream);
+/* in-place rotary embedding of the q and k parts of qkv [M, 3d]; position of
+ * row m = (m % rows_per_episode) + pos0 */
+DYQ_API dyq_status_t dyq_rope(uint16_t* qkv, int32_t M, int32_t rows_per_episode, int32_t pos0, int32_t d,
+                              int32_t n_heads, float theta, dyq_stream_t stream);
+/* causal self-attention of E episodes of S tokens (rows e*S + i of qkv / out);
+ * also writes K, V rows 0..S-1 of layer `layer` into the cache */
+DYQ_API dyq_status_t dyq_attention_prefill(const uint16_t* qkv, int32_t E, int32_t S, int32_t d,
+                                           int32_t n_heads, uint16_t* kv, int32_t layer, int32_t n_layers,
+                                           int32_t T, uint16_t* out, dyq_stream_t stream);
+/* one new token per episode at position pos: writes its K, V into the cache,
+ * attends over cache positions 0..pos */
+DYQ_API dyq_status_t dyq_attention_decode(const uint16_t* qkv, int32_t E, int32_t pos, int32_t d,
+                                          int32_t n_heads, uint16_t* kv, int32_t layer, int32_t n_layers,
+                                          int32_t T, uint16_t* out, dyq_stream_t stream);
+/* act[m, j] = SiLU(gu[m, j]) * gu[m, ffn + j] */
+DYQ_API dyq_status_t dyq_silu_mul(const uint16_t* gu, int32_t M, int32_t ffn, uint16_t* act,
+                                  dyq_stream_t stream);
+/* logits[e, b] = x[e*row_stride] . head_bins[b] (fp32); tok[e*tok_stride] = argmax_b (lowest b on ties) */
+DYQ_API dyq_status_t dyq_head_argmax(const uint16_t* x, int32_t E, int32_t row_stride, int32_t d,
+                                     const uint16_t* head_bins, int32_t n_bins, float* logits, int32_t* tok,
+                                     int32_t tok_stride, dyq_stream_t stream);
 
 #ifdef __cplusplus
 }

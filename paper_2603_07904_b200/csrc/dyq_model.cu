@@ -1,0 +1,600 @@
+// dyq_model.cu -- the policy step around the quantized linears (SURVEY.md §8(a)
+// A9): Llama-2 / OpenVLA block glue and the step orchestration
+// select_bits -> route -> prefill -> action head -> decode passes -> detok
+// (P:300-321).  The glue is not the paper's method: plain,
+// memory-bound kernels (RMSNorm, RoPE, SiLU*mul) and CUDA-core attention over
+// at most n_vis + n_text + n_act = 295 positions; every FLOP that matters
+// runs in the qlinear kernels (dyq_decode.cu / dyq_prefill.cu).
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "dyq_internal.cuh"
+#include "dyq_ptx.cuh"
+
+namespace dyq {
+
+constexpr int HD = 128;  // head dim (Llama-2-7B: 4096 / 32)
+
+__device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float((uint32_t)h << 16); }
+__device__ __forceinline__ uint16_t f2bf(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    float s = 0.f;
+    for (int i = 0; i < nw; ++i) s += red[i];
+    return s;
+}
+
+// h (+)= delta; y = RMSNorm(h) * w  (fp32 statistics over the bf16 h values)
+__global__ void add_rmsnorm_kernel(uint16_t* __restrict__ h, const uint16_t* __restrict__ delta,
+                                   const uint16_t* __restrict__ w, int d, float eps, uint16_t* __restrict__ y) {
+    __shared__ float red[32];
+    const size_t row = blockIdx.x;
+    uint16_t* hr = h + row * d;
+    float ss = 0.f;
+    for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2) {
+        float a = bf2f(hr[i]), b = bf2f(hr[i + 1]);
+        if (delta) {
+            a = bf2f(f2bf(a + bf2f(delta[row * d + i])));
+            b = bf2f(f2bf(b + bf2f(delta[row * d + i + 1])));
+            hr[i] = f2bf(a);
+            hr[i + 1] = f2bf(b);
+        }
+        ss += a * a + b * b;
+    }
+    const float inv = rsqrtf(block_sum(ss, red) / (float)d + eps);
+    for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2) {
+        y[row * d + i] = f2bf(bf2f(hr[i]) * inv * bf2f(w[i]));
+        y[row * d + i + 1] = f2bf(bf2f(hr[i + 1]) * inv * bf2f(w[i + 1]));
+    }
+}
+
+// rotate_half RoPE on the q and k parts: pairs (i, i + HD/2) of every head
+__global__ void rope_kernel(uint16_t* __restrict__ qkv, int M, int S, int pos0, int d, int H, float theta) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int half = HD / 2;
+    const size_t per_row = (size_t)2 * H * half;
+    if (idx >= (size_t)M * per_row) return;
+    const int m = (int)(idx / per_row);
+    const int r = (int)(idx % per_row);
+    const int which = r / (H * half);  // 0 = q, 1 = k
+    const int hh = (r / half) % H, i = r % half;
+    const float pos = (float)(m % S + pos0);
+    const float inv_freq = powf(theta, -2.f * (float)i / (float)HD);
+    float sn, cs;
+    sincosf(pos * inv_freq, &sn, &cs);
+    uint16_t* p = qkv + (size_t)m * 3 * d + (size_t)which * d + hh * HD;
+    const float x1 = bf2f(p[i]), x2 = bf2f(p[i + half]);
+    p[i] = f2bf(x1 * cs - x2 * sn);
+    p[i + half] = f2bf(x2 * cs + x1 * sn);
+}
+
+__device__ __forceinline__ size_t kv_off(int e, int l, int kv, int pos, int L, int T, int d) {
+    return ((((size_t)e * L + l) * 2 + kv) * T + pos) * d;
+}
+
+// Causal attention, prefill.  CTA = (32-query block, head, episode), 8 warps x
+// 4 queries.  K (rows padded to 130 bf16: conflict-free lane-per-key dot
+// products) and V of keys [0, qend) staged in shared memory.
+constexpr int AQB = 32;
+constexpr int AKP = HD + 2;
+__host__ __device__ inline size_t attn_ks_bytes(int S) { return ((size_t)S * AKP * 2 + 15) & ~(size_t)15; }
+__global__ void __launch_bounds__(256) attn_prefill_kernel(const uint16_t* __restrict__ qkv, int S, int d, int H,
+                                                           uint16_t* __restrict__ kv, int layer, int L, int T,
+                                                           uint16_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const int q0 = blockIdx.x * AQB, hh = blockIdx.y, e = blockIdx.z;
+    const int qend = min(q0 + AQB, S);
+    uint16_t* Ks = reinterpret_cast<uint16_t*>(sm);
+    uint16_t* Vs = reinterpret_cast<uint16_t*>(sm + attn_ks_bytes(S));
+    float* qs = reinterpret_cast<float*>(sm + attn_ks_bytes(S) + (size_t)S * HD * 2);  // [8][HD]
+    float* ps = qs + 8 * HD;                                                          // [8][S]
+    const size_t rs = (size_t)3 * d;
+    const uint16_t* base = qkv + (size_t)e * S * rs;
+    for (int idx = threadIdx.x; idx < qend * (HD / 2); idx += blockDim.x) {
+        const int j = idx / (HD / 2), c = (idx % (HD / 2)) * 2;
+        const uint32_t kk = *reinterpret_cast<const uint32_t*>(base + j * rs + d + hh * HD + c);
+        const uint32_t vv = *reinterpret_cast<const uint32_t*>(base + j * rs + 2 * d + hh * HD + c);
+        *reinterpret_cast<uint32_t*>(Ks + j * AKP + c) = kk;
+        *reinterpret_cast<uint32_t*>(Vs + j * HD + c) = vv;
+        if (j >= q0) {  // this block's rows go to the KV cache
+            *reinterpret_cast<uint32_t*>(kv + kv_off(e, layer, 0, j, L, T, d) + hh * HD + c) = kk;
+            *reinterpret_cast<uint32_t*>(kv + kv_off(e, layer, 1, j, L, T, d) + hh * HD + c) = vv;
+        }
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float scale = rsqrtf((float)HD);
+    float* qw = qs + warp * HD;
+    float* pw = ps + warp * S;
+    for (int qi = 0; qi < AQB / 8; ++qi) {
+        const int q = q0 + warp * (AQB / 8) + qi;
+        if (q >= qend) break;
+        for (int c = lane; c < HD; c += 32) qw[c] = bf2f(base[q * rs + hh * HD + c]) * scale;
+        __syncwarp();
+        float mx = -INFINITY;
+        for (int j = lane; j <= q; j += 32) {
+            const uint16_t* kr = Ks + j * AKP;
+            float s = 0.f;
+#pragma unroll 8
+            for (int c = 0; c < HD; c += 2) {
+                const uint32_t k2 = *reinterpret_cast<const uint32_t*>(kr + c);
+                s = fmaf(qw[c], __uint_as_float(k2 << 16), s);
+                s = fmaf(qw[c + 1], __uint_as_float(k2 & 0xffff0000u), s);
+            }
+            pw[j] = s;
+            mx = fmaxf(mx, s);
+        }
+        mx = warp_max(mx);
+        float sum = 0.f;
+        for (int j = lane; j <= q; j += 32) {
+            const float p = __expf(pw[j] - mx);
+            pw[j] = p;
+            sum += p;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        __syncwarp();
+        float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+        for (int j = 0; j <= q; ++j) {
+            const float p = pw[j];
+            const uint2 v = *reinterpret_cast<const uint2*>(Vs + j * HD + lane * 4);
+            o0 = fmaf(p, __uint_as_float(v.x << 16), o0);
+            o1 = fmaf(p, __uint_as_float(v.x & 0xffff0000u), o1);
+            o2 = fmaf(p, __uint_as_float(v.y << 16), o2);
+            o3 = fmaf(p, __uint_as_float(v.y & 0xffff0000u), o3);
+        }
+        const float inv = 1.f / sum;
+        uint16_t* orow = out + ((size_t)e * S + q) * d + hh * HD + lane * 4;
+        orow[0] = f2bf(o0 * inv);
+        orow[1] = f2bf(o1 * inv);
+        orow[2] = f2bf(o2 * inv);
+        orow[3] = f2bf(o3 * inv);
+        __syncwarp();
+    }
+}
+
+// Decode attention: CTA = (head, episode); the new token's K, V are written to
+// the cache at `pos`, then softmax(q K^T) V over positions 0..pos.
+__global__ void __launch_bounds__(256) attn_decode_kernel(const uint16_t* __restrict__ qkv, int pos, int d, int H,
+                                                          uint16_t* __restrict__ kv, int layer, int L, int T,
+                                                          uint16_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    float* qsh = reinterpret_cast<float*>(sm);  // [HD]
+    float* ps = qsh + HD;                        // [pos + 1]
+    float* red = ps + (pos + 1);                 // [32]
+    float* part = red + 32;                      // [4][HD]
+    const int hh = blockIdx.x, e = blockIdx.y;
+    const size_t rs = (size_t)3 * d;
+    const uint16_t* row = qkv + (size_t)e * rs;
+    uint16_t* Kc = kv + kv_off(e, layer, 0, 0, L, T, d) + hh * HD;
+    uint16_t* Vc = kv + kv_off(e, layer, 1, 0, L, T, d) + hh * HD;
+    const float scale = rsqrtf((float)HD);
+    for (int c = threadIdx.x; c < HD; c += blockDim.x) {
+        Kc[(size_t)pos * d + c] = row[d + hh * HD + c];
+        Vc[(size_t)pos * d + c] = row[2 * d + hh * HD + c];
+        qsh[c] = bf2f(row[hh * HD + c]) * scale;
+    }
+    __syncthreads();
+    float mx = -INFINITY;
+    for (int j = threadIdx.x; j <= pos; j += blockDim.x) {
+        const uint16_t* kr = Kc + (size_t)j * d;
+        float s = 0.f;
+#pragma unroll 4
+        for (int c = 0; c < HD; c += 8) {
+            const uint4 k8 = *reinterpret_cast<const uint4*>(kr + c);
+            const uint32_t kk[4] = {k8.x, k8.y, k8.z, k8.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                s = fmaf(qsh[c + 2 * u], __uint_as_float(kk[u] << 16), s);
+                s = fmaf(qsh[c + 2 * u + 1], __uint_as_float(kk[u] & 0xffff0000u), s);
+            }
+        }
+        ps[j] = s;
+        mx = fmaxf(mx, s);
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, red[i]);
+    __syncthreads();
+    float sum = 0.f;
+    for (int j = threadIdx.x; j <= pos; j += blockDim.x) {
+        const float p = __expf(ps[j] - mx);
+        ps[j] = p;
+        sum += p;
+    }
+    sum = block_sum(sum, red);  // (contains the barrier that publishes ps)
+    // o[c] over keys: thread = (dim pair, key quarter)
+    const int c2 = (threadIdx.x & 63) * 2, qt = threadIdx.x >> 6;
+    float o0 = 0.f, o1 = 0.f;
+    for (int j = qt; j <= pos; j += 4) {
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(Vc + (size_t)j * d + c2);
+        o0 = fmaf(ps[j], __uint_as_float(v << 16), o0);
+        o1 = fmaf(ps[j], __uint_as_float(v & 0xffff0000u), o1);
+    }
+    part[qt * HD + c2] = o0;
+    part[qt * HD + c2 + 1] = o1;
+    __syncthreads();
+    if (threadIdx.x < HD) {
+        const float o = part[threadIdx.x] + part[HD + threadIdx.x] + part[2 * HD + threadIdx.x] +
+                        part[3 * HD + threadIdx.x];
+        out[(size_t)e * d + hh * HD + threadIdx.x] = f2bf(o / sum);
+    }
+}
+
+__global__ void silu_mul_kernel(const uint16_t* __restrict__ gu, int M, int ffn, uint16_t* __restrict__ act) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)M * ffn) return;
+    const size_t m = idx / ffn, j = idx % ffn;
+    const float g = bf2f(gu[m * 2 * ffn + j]), u = bf2f(gu[m * 2 * ffn + ffn + j]);
+    act[idx] = f2bf(g / (1.f + __expf(-g)) * u);
+}
+
+// One CTA per episode: fp32 logits over the n_bins action-bin rows, argmax.
+__global__ void head_argmax_kernel(const uint16_t* __restrict__ x, int row_stride, int d,
+                                   const uint16_t* __restrict__ W, int n_bins, float* __restrict__ logits,
+                                   int32_t* __restrict__ tok, int tok_stride) {
+    extern __shared__ __align__(16) float xs[];  // [d]
+    __shared__ float bv[32];
+    __shared__ int bi[32];
+    const int e = blockIdx.x;
+    const uint16_t* xr = x + (size_t)e * row_stride * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) xs[i] = bf2f(xr[i]);
+    __syncthreads();
+    float best = -INFINITY;
+    int bidx = 0x7fffffff;
+    for (int b = threadIdx.x; b < n_bins; b += blockDim.x) {
+        const uint16_t* wr = W + (size_t)b * d;
+        float s = 0.f;
+        for (int i = 0; i < d; i += 8) {
+            const uint4 w8 = *reinterpret_cast<const uint4*>(wr + i);
+            const uint32_t ww[4] = {w8.x, w8.y, w8.z, w8.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                s = fmaf(xs[i + 2 * u], __uint_as_float(ww[u] << 16), s);
+                s = fmaf(xs[i + 2 * u + 1], __uint_as_float(ww[u] & 0xffff0000u), s);
+            }
+        }
+        if (logits) logits[(size_t)e * n_bins + b] = s;
+        if (s > best || (s == best && b < bidx)) { best = s; bidx = b; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+        if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = bidx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        best = bv[0];
+        bidx = bi[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (bv[w] > best || (bv[w] == best && bi[w] < bidx)) { best = bv[w]; bidx = bi[w]; }
+        tok[(size_t)e * tok_stride] = bidx;
+    }
+}
+
+// h rows of the prefill sequence: vision embeddings, then text-token embeddings
+__global__ void embed_prefill_kernel(const uint16_t* __restrict__ vis, const int32_t* __restrict__ text,
+                                     const uint16_t* __restrict__ embed, int n_vis, int n_text, int d,
+                                     uint16_t* __restrict__ h) {
+    const int S = n_vis + n_text;
+    const int row = blockIdx.x;  // e * S + i
+    const int e = row / S, i = row % S;
+    const uint16_t* src = i < n_vis ? vis + ((size_t)e * n_vis + i) * d
+                                    : embed + (size_t)text[(size_t)e * n_text + (i - n_vis)] * d;
+    for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8)
+        *reinterpret_cast<uint4*>(h + (size_t)row * d + c) = *reinterpret_cast<const uint4*>(src + c);
+}
+
+// decode input: embedding of the previous action token (vocab id vocab - n_bins + bin)
+__global__ void embed_action_kernel(const int32_t* __restrict__ tok, int n_act, int t, const uint16_t* __restrict__ embed,
+                                    int vocab, int n_bins, int d, uint16_t* __restrict__ h) {
+    const int e = blockIdx.x;
+    const int id = vocab - n_bins + tok[(size_t)e * n_act + t];
+    for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8)
+        *reinterpret_cast<uint4*>(h + (size_t)e * d + c) = *reinterpret_cast<const uint4*>(embed + (size_t)id * d + c);
+}
+
+__global__ void detok_kernel(const int32_t* __restrict__ tok, int E, int n_act, int n_bins, float* __restrict__ act,
+                             float* __restrict__ prev, const int32_t* __restrict__ bits, int32_t* __restrict__ bits_out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < E * n_act) {
+        const float v = -1.f + (2.f * (float)tok[i] + 1.f) / (float)n_bins;
+        act[i] = v;
+        // the kinematic proxies read a_{t-1} as [E, 7] (x,y,z, rx,ry,rz, grip)
+        const int e = i / n_act, k = i % n_act;
+        if (k < 7) prev[e * 7 + k] = v;
+    }
+    if (bits_out && i < E) bits_out[i] = bits[i];
+}
+
+// ------------------------------------------------------------------ host
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct ModelLayout {
+    int S, T, MP;
+    size_t h, xn, delta, att, qkv, gu, act, ws[4], rbp, rbd, bits, tok, prev, logits, err, total;
+    size_t ws_bytes[4], kv_bytes;  // one qlinear workspace per linear shape (split-K counters are per shape)
+};
+
+static dyq_wdesc_t wdesc_of(const dyq_model_desc_t& m, int which) {
+    dyq_wdesc_t w{};
+    w.group = m.group;
+    w.wbits = m.wbits;
+    w.round_mode = 0;
+    switch (which) {
+        case 0: w.N = 3 * m.d; w.K = m.d; break;
+        case 1: w.N = m.d; w.K = m.d; break;
+        case 2: w.N = 2 * m.ffn; w.K = m.d; break;
+        default: w.N = m.d; w.K = m.ffn; break;
+    }
+    return w;
+}
+
+static dyq_status_t model_layout(const dyq_model_desc_t* m, ModelLayout* L) {
+    if (!m) return set_error(DYQ_EINVAL, "null model descriptor");
+    if (m->n_layers <= 0 || m->d <= 0 || m->ffn <= 0 || m->n_heads <= 0 || m->E <= 0 || m->vocab <= 0)
+        return set_error(DYQ_EINVAL, "model dimensions must be positive");
+    if (m->d != m->n_heads * HD) return set_error(DYQ_EUNSUPPORTED, "head dim must be %d (d = n_heads * %d)", HD, HD);
+    if (m->d % 16 || m->ffn % 16) return set_error(DYQ_ESHAPE, "d and ffn must be multiples of 16");
+    if (m->n_vis < 0 || m->n_text < 1 || m->n_act < 1 || m->n_act > 7 + 64 || m->n_bins < 1 || m->n_bins > m->vocab)
+        return set_error(DYQ_EINVAL, "bad token counts");
+    if (m->n_act < 7) return set_error(DYQ_EINVAL, "n_act must be >= 7 (the kinematic proxies read a 7-dof action)");
+    L->S = m->n_vis + m->n_text;
+    L->T = L->S + m->n_act;
+    L->MP = m->E * L->S;
+    if (L->MP > 65536) return set_error(DYQ_ESHAPE, "E * (n_vis + n_text) must be <= 65536");
+    const size_t MP = L->MP, d = m->d, ffn = m->ffn;
+    for (int which = 0; which < 4; ++which) {
+        const dyq_wdesc_t w = wdesc_of(*m, which);
+        size_t wsb = 0;
+        for (int M : {L->MP, m->E}) {
+            size_t b = 0;
+            dyq_status_t rc = dyq_qlinear_workspace(&w, M, &b);
+            if (rc) return rc;
+            wsb = b > wsb ? b : wsb;
+        }
+        L->ws_bytes[which] = wsb;
+    }
+    size_t o = 0;
+    auto take = [&](size_t bytes) { const size_t r = o; o += al256(bytes); return r; };
+    L->h = take(MP * d * 2);
+    L->xn = take(MP * d * 2);
+    L->delta = take(MP * d * 2);
+    L->att = take(MP * d * 2);
+    L->qkv = take(MP * 3 * d * 2);
+    L->gu = take(MP * 2 * ffn * 2);
+    L->act = take(MP * ffn * 2);
+    for (int which = 0; which < 4; ++which) L->ws[which] = take(L->ws_bytes[which]);
+    L->rbp = take(MP * 4);
+    L->rbd = take((size_t)m->E * 4);
+    L->bits = take((size_t)m->E * 4);
+    L->tok = take((size_t)m->E * m->n_act * 4);
+    L->prev = take((size_t)m->E * 7 * 4);
+    L->logits = take((size_t)m->E * m->n_bins * 4);
+    L->err = take(8);
+    L->total = o;
+    L->kv_bytes = (size_t)m->E * m->n_layers * 2 * L->T * d * 2;
+    return DYQ_OK;
+}
+
+struct Model {
+    dyq_model_desc_t d;
+    std::vector<const void*> codes, meta;
+    ModelLayout L;
+    int t = 0;
+    uint8_t* sb() const { return reinterpret_cast<uint8_t*>(d.scratch); }
+    template <class T>
+    T* at(size_t off) const { return reinterpret_cast<T*>(sb() + off); }
+};
+
+}  // namespace dyq
+
+using namespace dyq;
+
+extern "C" {
+
+dyq_status_t dyq_add_rmsnorm(uint16_t* h, const uint16_t* delta, const uint16_t* w, int32_t M, int32_t d, float eps,
+                             uint16_t* y, dyq_stream_t stream) {
+    if (M < 0 || d <= 0 || d % 2) return set_error(DYQ_ESHAPE, "bad rmsnorm shape");
+    if (M == 0) return DYQ_OK;
+    if (!h || !w || !y) return set_error(DYQ_EINVAL, "null pointer");
+    add_rmsnorm_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(h, delta, w, d, eps, y);
+    return check_launch("add_rmsnorm_kernel");
+}
+
+dyq_status_t dyq_rope(uint16_t* qkv, int32_t M, int32_t S, int32_t pos0, int32_t d, int32_t H, float theta,
+                      dyq_stream_t stream) {
+    if (M < 0 || S <= 0 || d != H * HD) return set_error(DYQ_ESHAPE, "bad rope shape (head dim %d)", HD);
+    if (M == 0) return DYQ_OK;
+    const size_t n = (size_t)M * 2 * H * (HD / 2);
+    rope_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(qkv, M, S, pos0, d, H, theta);
+    return check_launch("rope_kernel");
+}
+
+dyq_status_t dyq_attention_prefill(const uint16_t* qkv, int32_t E, int32_t S, int32_t d, int32_t H, uint16_t* kv,
+                                   int32_t layer, int32_t L, int32_t T, uint16_t* out, dyq_stream_t stream) {
+    if (E <= 0 || S <= 0 || S > T || d != H * HD || layer < 0 || layer >= L)
+        return set_error(DYQ_ESHAPE, "bad attention shape");
+    const size_t smem = attn_ks_bytes(S) + (size_t)S * HD * 2 + 8 * HD * 4 + (size_t)8 * S * 4;
+    if (smem > 227 * 1024) return set_error(DYQ_EUNSUPPORTED, "attention prefill: S = %d too long", S);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(attn_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    const dim3 grid((S + AQB - 1) / AQB, H, E);
+    attn_prefill_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(qkv, S, d, H, kv, layer, L, T, out);
+    return check_launch("attn_prefill_kernel");
+}
+
+dyq_status_t dyq_attention_decode(const uint16_t* qkv, int32_t E, int32_t pos, int32_t d, int32_t H, uint16_t* kv,
+                                  int32_t layer, int32_t L, int32_t T, uint16_t* out, dyq_stream_t stream) {
+    if (E <= 0 || pos < 0 || pos >= T || d != H * HD || layer < 0 || layer >= L)
+        return set_error(DYQ_ESHAPE, "bad attention shape");
+    const size_t smem = (HD + (size_t)(pos + 1) + 32 + 4 * HD) * 4;
+    attn_decode_kernel<<<dim3(H, E), 256, smem, (cudaStream_t)stream>>>(qkv, pos, d, H, kv, layer, L, T, out);
+    return check_launch("attn_decode_kernel");
+}
+
+dyq_status_t dyq_silu_mul(const uint16_t* gu, int32_t M, int32_t ffn, uint16_t* act, dyq_stream_t stream) {
+    if (M < 0 || ffn <= 0) return set_error(DYQ_ESHAPE, "bad silu_mul shape");
+    if (M == 0) return DYQ_OK;
+    const size_t n = (size_t)M * ffn;
+    silu_mul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(gu, M, ffn, act);
+    return check_launch("silu_mul_kernel");
+}
+
+dyq_status_t dyq_head_argmax(const uint16_t* x, int32_t E, int32_t row_stride, int32_t d, const uint16_t* W,
+                             int32_t n_bins, float* logits, int32_t* tok, int32_t tok_stride, dyq_stream_t stream) {
+    if (E <= 0 || d <= 0 || d % 8 || n_bins <= 0) return set_error(DYQ_ESHAPE, "bad head shape");
+    head_argmax_kernel<<<E, 256, (size_t)d * 4, (cudaStream_t)stream>>>(x, row_stride, d, W, n_bins, logits, tok,
+                                                                          tok_stride);
+    return check_launch("head_argmax_kernel");
+}
+
+dyq_status_t dyq_model_size(const dyq_model_desc_t* desc, size_t* kv_bytes, size_t* scratch_bytes) {
+    ModelLayout L;
+    dyq_status_t rc = model_layout(desc, &L);
+    if (rc) return rc;
+    if (kv_bytes) *kv_bytes = L.kv_bytes;
+    if (scratch_bytes) *scratch_bytes = L.total;
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_model_bind(const dyq_model_desc_t* desc, void** model) {
+    if (!model) return set_error(DYQ_EINVAL, "null output handle");
+    ModelLayout L;
+    dyq_status_t rc = model_layout(desc, &L);
+    if (rc) return rc;
+    if (!desc->codes || !desc->meta || !desc->attn_norm || !desc->mlp_norm || !desc->final_norm || !desc->embed ||
+        !desc->head_bins || !desc->kv || !desc->scratch)
+        return set_error(DYQ_EINVAL, "null pointer in model descriptor");
+    Model* m = new Model();
+    m->d = *desc;
+    m->codes.assign(desc->codes, desc->codes + 4 * desc->n_layers);
+    m->meta.assign(desc->meta, desc->meta + 4 * desc->n_layers);
+    for (int i = 0; i < 4 * desc->n_layers; ++i)
+        if (!m->codes[i] || !m->meta[i]) {
+            delete m;
+            return set_error(DYQ_EINVAL, "null packed-weight pointer for linear %d", i);
+        }
+    m->d.codes = nullptr;
+    m->d.meta = nullptr;
+    m->L = L;
+    *model = m;
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_model_init(void* model, dyq_stream_t stream) {
+    Model* m = reinterpret_cast<Model*>(model);
+    if (!m) return set_error(DYQ_EINVAL, "null model");
+    m->t = 0;
+    if (cudaMemsetAsync(m->d.scratch, 0, m->L.total, (cudaStream_t)stream) != cudaSuccess)
+        return check_launch("dyq_model_init");
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_model_free(void* model) {
+    delete reinterpret_cast<Model*>(model);
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t* vis, const int32_t* text,
+                             float* action_out, int32_t* bits_out, dyq_stream_t stream) {
+    Model* m = reinterpret_cast<Model*>(model);
+    if (!m || !state || !vis || !text || !action_out) return set_error(DYQ_EINVAL, "null pointer");
+    const dyq_model_desc_t& D = m->d;
+    const ModelLayout& L = m->L;
+    if (E <= 0 || E > D.E) return set_error(DYQ_EINVAL, "E = %d outside [1, %d]", E, D.E);
+    const int S = L.S, d = D.d, ffn = D.ffn, H = D.n_heads, NL = D.n_layers;
+    const int MP = E * S;
+    uint16_t* h = m->at<uint16_t>(L.h);
+    uint16_t* xn = m->at<uint16_t>(L.xn);
+    uint16_t* delta = m->at<uint16_t>(L.delta);
+    uint16_t* att = m->at<uint16_t>(L.att);
+    uint16_t* qkv = m->at<uint16_t>(L.qkv);
+    uint16_t* gu = m->at<uint16_t>(L.gu);
+    uint16_t* act = m->at<uint16_t>(L.act);
+    void* ws[4];
+    for (int i = 0; i < 4; ++i) ws[i] = m->at<uint8_t>(L.ws[i]);
+    int32_t* rbp = m->at<int32_t>(L.rbp);
+    int32_t* rbd = m->at<int32_t>(L.rbd);
+    int32_t* bits = m->at<int32_t>(L.bits);
+    int32_t* tok = m->at<int32_t>(L.tok);
+    float* prev = m->at<float>(L.prev);
+    float* logits = m->at<float>(L.logits);
+    int64_t* err = m->at<int64_t>(L.err);
+    uint16_t* kv = reinterpret_cast<uint16_t*>(D.kv);
+    const cudaStream_t st = (cudaStream_t)stream;
+    dyq_status_t rc;
+#define DYQ_TRY(x)        \
+    do {                  \
+        rc = (x);         \
+        if (rc) return rc; \
+    } while (0)
+    dyq_wdesc_t wd[4];
+    for (int i = 0; i < 4; ++i) wd[i] = wdesc_of(D, i);
+
+    // b*_t from a_{t-1}, then per-row activation bits (W4-pinned table)
+    DYQ_TRY(dyq_select_bits(state, E, m->t == 0 ? nullptr : prev, bits, nullptr, nullptr, stream));
+    DYQ_TRY(dyq_route_bits(bits, E, S, nullptr, rbp, stream));
+    DYQ_TRY(dyq_route_bits(bits, E, 1, nullptr, rbd, stream));
+
+    auto layer = [&](int l, int M, int32_t* rb, bool prefill, int pos) -> dyq_status_t {
+        const size_t li = (size_t)4 * l;
+        DYQ_TRY(dyq_qlinear(&wd[0], m->codes[li], m->meta[li], xn, M, rb, 0, qkv, 1, ws[0], L.ws_bytes[0], err,
+                            stream));
+        DYQ_TRY(dyq_rope(qkv, M, prefill ? S : 1, prefill ? 0 : pos, d, H, D.rope_theta, stream));
+        if (prefill)
+            DYQ_TRY(dyq_attention_prefill(qkv, E, S, d, H, kv, l, NL, L.T, att, stream));
+        else
+            DYQ_TRY(dyq_attention_decode(qkv, E, pos, d, H, kv, l, NL, L.T, att, stream));
+        DYQ_TRY(dyq_qlinear(&wd[1], m->codes[li + 1], m->meta[li + 1], att, M, rb, 0, delta, 1, ws[1], L.ws_bytes[1],
+                            err, stream));
+        DYQ_TRY(dyq_add_rmsnorm(h, delta, D.mlp_norm + (size_t)l * d, M, d, D.rms_eps, xn, stream));
+        DYQ_TRY(dyq_qlinear(&wd[2], m->codes[li + 2], m->meta[li + 2], xn, M, rb, 0, gu, 1, ws[2], L.ws_bytes[2],
+                            err, stream));
+        DYQ_TRY(dyq_silu_mul(gu, M, ffn, act, stream));
+        DYQ_TRY(dyq_qlinear(&wd[3], m->codes[li + 3], m->meta[li + 3], act, M, rb, 0, delta, 1, ws[3], L.ws_bytes[3],
+                            err, stream));
+        const uint16_t* nw = l + 1 < NL ? D.attn_norm + (size_t)(l + 1) * d : D.final_norm;
+        DYQ_TRY(dyq_add_rmsnorm(h, delta, nw, M, d, D.rms_eps, xn, stream));
+        return DYQ_OK;
+    };
+
+    // ---- prefill: vision + text tokens
+    embed_prefill_kernel<<<MP, 128, 0, st>>>(vis, text, D.embed, D.n_vis, D.n_text, d, h);
+    DYQ_TRY(check_launch("embed_prefill_kernel"));
+    DYQ_TRY(dyq_add_rmsnorm(h, nullptr, D.attn_norm, MP, d, D.rms_eps, xn, stream));
+    for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, MP, rbp, true, 0));
+    DYQ_TRY(dyq_head_argmax(xn + (size_t)(S - 1) * d, E, S, d, D.head_bins, D.n_bins, logits, tok, D.n_act, stream));
+    // ---- decode passes: one action token per pass
+    for (int t = 1; t < D.n_act; ++t) {
+        embed_action_kernel<<<E, 128, 0, st>>>(tok, D.n_act, t - 1, D.embed, D.vocab, D.n_bins, d, h);
+        DYQ_TRY(check_launch("embed_action_kernel"));
+        DYQ_TRY(dyq_add_rmsnorm(h, nullptr, D.attn_norm, E, d, D.rms_eps, xn, stream));
+        for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, E, rbd, false, S + t - 1));
+        DYQ_TRY(dyq_head_argmax(xn, E, 1, d, D.head_bins, D.n_bins, logits, tok + t, D.n_act, stream));
+    }
+    detok_kernel<<<(E * D.n_act + 127) / 128, 128, 0, st>>>(tok, E, D.n_act, D.n_bins, action_out, prev, bits,
+                                                             bits_out);
+    DYQ_TRY(check_launch("detok_kernel"));
+#undef DYQ_TRY
+    m->t += 1;
+    return DYQ_OK;
+}
+
+}  // extern "C"

@@ -39,6 +39,17 @@ _SIGS = {
     "dyq_set_path": [i32],
     "dyq_act_quant": [P, P, i32, P, i32, P, sz, P, P],
     "dyq_qlinear_q": [P, P, P, P, i32, P, i32, P, i32, P, sz, P],
+    "dyq_model_size": [P, P, P],
+    "dyq_model_bind": [P, P],
+    "dyq_model_init": [P, P],
+    "dyq_model_free": [P],
+    "dyq_policy_step": [P, P, i32, P, P, P, P, P],
+    "dyq_add_rmsnorm": [P, P, P, i32, i32, C.c_float, P, P],
+    "dyq_rope": [P, i32, i32, i32, i32, i32, C.c_float, P],
+    "dyq_attention_prefill": [P, i32, i32, i32, i32, P, i32, i32, i32, P, P],
+    "dyq_attention_decode": [P, i32, i32, i32, i32, P, i32, i32, i32, P, P],
+    "dyq_silu_mul": [P, i32, i32, P, P],
+    "dyq_head_argmax": [P, i32, i32, i32, P, i32, P, P, i32, P],
 }
 _RESTYPES = {"dyq_last_error": C.c_char_p, "dyq_version": C.c_char_p}
 
@@ -255,3 +266,94 @@ class PackedLinear:
         qlinear(self.wd, self.codes, self.meta, x, M, row_bits, bits, y,
                 0 if out_dtype == torch.float32 else 1, ws, err, stream)
         return y
+
+
+# ------------------------------------------------------------- policy step
+class ModelDesc(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("d", C.c_int32), ("ffn", C.c_int32), ("n_heads", C.c_int32),
+                ("vocab", C.c_int32), ("E", C.c_int32), ("n_vis", C.c_int32), ("n_text", C.c_int32),
+                ("n_act", C.c_int32), ("n_bins", C.c_int32), ("group", C.c_int32), ("wbits", C.c_int32),
+                ("rms_eps", C.c_float), ("rope_theta", C.c_float),
+                ("codes", C.POINTER(C.c_void_p)), ("meta", C.POINTER(C.c_void_p)),
+                ("attn_norm", C.c_void_p), ("mlp_norm", C.c_void_p), ("final_norm", C.c_void_p),
+                ("embed", C.c_void_p), ("head_bins", C.c_void_p), ("kv", C.c_void_p), ("scratch", C.c_void_p)]
+
+
+def add_rmsnorm(h, delta, w, M: int, d: int, eps: float, y, stream=None):
+    _call("dyq_add_rmsnorm", _ptr(h), _ptr(delta), _ptr(w), M, d, eps, _ptr(y), _stream(stream))
+
+
+def rope(qkv, M: int, rows_per_episode: int, pos0: int, d: int, n_heads: int, theta: float, stream=None):
+    _call("dyq_rope", _ptr(qkv), M, rows_per_episode, pos0, d, n_heads, theta, _stream(stream))
+
+
+def attention_prefill(qkv, E: int, S: int, d: int, n_heads: int, kv, layer: int, n_layers: int, T: int, out,
+                      stream=None):
+    _call("dyq_attention_prefill", _ptr(qkv), E, S, d, n_heads, _ptr(kv), layer, n_layers, T, _ptr(out),
+          _stream(stream))
+
+
+def attention_decode(qkv, E: int, pos: int, d: int, n_heads: int, kv, layer: int, n_layers: int, T: int, out,
+                     stream=None):
+    _call("dyq_attention_decode", _ptr(qkv), E, pos, d, n_heads, _ptr(kv), layer, n_layers, T, _ptr(out),
+          _stream(stream))
+
+
+def silu_mul(gu, M: int, ffn: int, act, stream=None):
+    _call("dyq_silu_mul", _ptr(gu), M, ffn, _ptr(act), _stream(stream))
+
+
+def head_argmax(x, E: int, row_stride: int, d: int, head_bins, n_bins: int, logits, tok, tok_stride: int,
+                stream=None):
+    _call("dyq_head_argmax", _ptr(x), E, row_stride, d, _ptr(head_bins), n_bins, _ptr(logits), _ptr(tok),
+          tok_stride, _stream(stream))
+
+
+class Model:
+    """A bound policy-step model: packed linears + bf16 glue weights, caller-
+    owned KV cache and scratch (torch tensors).  `layers` = list of n_layers
+    lists [qkv, o, gate_up, down] of PackedLinear."""
+
+    def __init__(self, layers, attn_norm, mlp_norm, final_norm, embed, head_bins, E: int,
+                 n_heads: int = 32, n_vis: int = 256, n_text: int = 32, n_act: int = 7,
+                 rms_eps: float = 1e-5, rope_theta: float = 10000.0, stream=None):
+        import torch
+        qkv0 = layers[0][0].wd
+        d = qkv0.K
+        ffn = layers[0][2].wd.N // 2
+        self._keep = [layers, attn_norm, mlp_norm, final_norm, embed, head_bins]
+        nl = len(layers)
+        self._codes = (C.c_void_p * (4 * nl))(*[l.codes.data_ptr() for L in layers for l in L])
+        self._meta = (C.c_void_p * (4 * nl))(*[l.meta.data_ptr() for L in layers for l in L])
+        self.desc = ModelDesc(nl, d, ffn, n_heads, embed.shape[0], E, n_vis, n_text, n_act, head_bins.shape[0],
+                              qkv0.group, qkv0.wbits, rms_eps, rope_theta,
+                              C.cast(self._codes, C.POINTER(C.c_void_p)), C.cast(self._meta, C.POINTER(C.c_void_p)),
+                              attn_norm.data_ptr(), mlp_norm.data_ptr(), final_norm.data_ptr(), embed.data_ptr(),
+                              head_bins.data_ptr(), None, None)
+        kvb, scb = C.c_size_t(0), C.c_size_t(0)
+        _call("dyq_model_size", C.byref(self.desc), C.byref(kvb), C.byref(scb))
+        dev = embed.device
+        self.kv = torch.zeros(kvb.value // 2, dtype=torch.int16, device=dev)
+        self.scratch = torch.zeros(scb.value, dtype=torch.uint8, device=dev)
+        self.desc.kv = self.kv.data_ptr()
+        self.desc.scratch = self.scratch.data_ptr()
+        self._h = C.c_void_p()
+        _call("dyq_model_bind", C.byref(self.desc), C.byref(self._h))
+        _call("dyq_model_init", self._h, _stream(stream))
+        self.E, self.n_act, self.T = E, n_act, n_vis + n_text + n_act
+
+    def init(self, stream=None):
+        _call("dyq_model_init", self._h, _stream(stream))
+
+    def step(self, state, E: int, vis_emb, text_ids, action_out, bits_out=None, stream=None):
+        _call("dyq_policy_step", self._h, _ptr(state), E, _ptr(vis_emb), _ptr(text_ids), _ptr(action_out),
+              _ptr(bits_out), _stream(stream))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().dyq_model_free(h)
+            except Exception:
+                pass
+            self._h = None

@@ -1,0 +1,209 @@
+"""GPU parity of the policy-step glue kernels and of dyq_policy_step
+against oracle/glue.py (numpy) and the C oracle's qlinear / bit selection."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import glue
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2603_07904_b200 import dyq  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def t16(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.uint16).view(np.int16)).to(DEV)
+
+
+def f64(t):
+    return glue.from_bf16_bits(t.cpu().numpy().view(np.uint16))
+
+
+def close_bf16(got, ref, rtol=2e-2, floor=1e-2):
+    scale = np.maximum(np.abs(ref), floor * np.abs(ref).max())
+    err = np.abs(got - ref) / scale
+    assert err.max() <= rtol, f"max rel err {err.max():.3g} at {np.unravel_index(err.argmax(), err.shape)}"
+
+
+def rnd_bits(shape, seed, scale=1.0):
+    return glue.to_bf16_bits(np.random.default_rng(seed).standard_normal(shape) * scale)
+
+
+@pytest.mark.parametrize("M,d", [(1, 256), (7, 4096), (33, 512)])
+@pytest.mark.parametrize("with_delta", [False, True])
+def test_add_rmsnorm(M, d, with_delta):
+    h0, de, w = rnd_bits((M, d), 1), rnd_bits((M, d), 2, 0.5), rnd_bits(d, 3, 0.2) + 0
+    w = glue.to_bf16_bits(1.0 + glue.from_bf16_bits(rnd_bits(d, 3, 0.2)))
+    h, y = t16(h0), torch.empty(M, d, dtype=torch.int16, device=DEV)
+    dyq.add_rmsnorm(h, t16(de) if with_delta else None, t16(w), M, d, 1e-5, y)
+    hr = glue.from_bf16_bits(h0)
+    if with_delta:
+        hr = glue.bf16_round(hr + glue.from_bf16_bits(de))
+        assert np.array_equal(f64(h), hr)
+    close_bf16(f64(y), glue.rmsnorm(hr, glue.from_bf16_bits(w), 1e-5))
+
+
+@pytest.mark.parametrize("M,S,pos0", [(12, 12, 0), (3, 1, 295), (20, 10, 0)])
+def test_rope(M, S, pos0):
+    d = 512
+    x0 = rnd_bits((M, 3 * d), 4)
+    x = t16(x0)
+    dyq.rope(x, M, S, pos0, d, 4, 10000.0)
+    pos = np.arange(M) % S + pos0
+    xr = glue.from_bf16_bits(x0)
+    got = f64(x)
+    close_bf16(got[:, :d], glue.rope(xr[:, :d], pos, 10000.0))
+    close_bf16(got[:, d:2 * d], glue.rope(xr[:, d:2 * d], pos, 10000.0))
+    assert np.array_equal(got[:, 2 * d:], xr[:, 2 * d:])  # V untouched
+
+
+@pytest.mark.parametrize("E,S", [(1, 288), (2, 45), (3, 7)])
+def test_attention_prefill_and_cache(E, S):
+    d, H, L, T = 256, 2, 3, S + 7
+    qkv0 = rnd_bits((E * S, 3 * d), 5)
+    kv = torch.zeros(E * L * 2 * T * d, dtype=torch.int16, device=DEV)
+    out = torch.empty(E * S, d, dtype=torch.int16, device=DEV)
+    dyq.attention_prefill(t16(qkv0), E, S, d, H, kv, 1, L, T, out)
+    x = glue.from_bf16_bits(qkv0)
+    kvh = kv.cpu().numpy().view(np.uint16).reshape(E, L, 2, T, d)
+    got = f64(out)
+    for e in range(E):
+        r = slice(e * S, (e + 1) * S)
+        ref = glue.attention(x[r, :d], x[r, d:2 * d], x[r, 2 * d:], causal=True)
+        close_bf16(got[r], ref)
+        assert np.array_equal(glue.from_bf16_bits(kvh[e, 1, 0, :S]), x[r, d:2 * d])
+        assert np.array_equal(glue.from_bf16_bits(kvh[e, 1, 1, :S]), x[r, 2 * d:])
+        assert not kvh[e, 0].any() and not kvh[e, 2].any()
+
+
+@pytest.mark.parametrize("E,pos", [(1, 0), (2, 100), (4, 294)])
+def test_attention_decode(E, pos):
+    d, H, L, T = 256, 2, 2, 295
+    rng = np.random.default_rng(6)
+    kvh = glue.to_bf16_bits(rng.standard_normal((E, L, 2, T, d)))
+    kv = t16(kvh.reshape(-1))
+    qkv0 = rnd_bits((E, 3 * d), 7)
+    out = torch.empty(E, d, dtype=torch.int16, device=DEV)
+    dyq.attention_decode(t16(qkv0), E, pos, d, H, kv, 1, L, T, out)
+    x = glue.from_bf16_bits(qkv0)
+    kvg = kv.cpu().numpy().view(np.uint16).reshape(E, L, 2, T, d)
+    for e in range(E):
+        K = glue.from_bf16_bits(kvh[e, 1, 0, :pos + 1]).copy()
+        V = glue.from_bf16_bits(kvh[e, 1, 1, :pos + 1]).copy()
+        K[pos], V[pos] = x[e, d:2 * d], x[e, 2 * d:]
+        ref = glue.attention(x[e:e + 1, :d], K, V, causal=False)
+        close_bf16(f64(out)[e:e + 1], ref)
+        assert np.array_equal(kvg[e, 1, 0, pos], glue.to_bf16_bits(x[e, d:2 * d]))
+
+
+def test_silu_mul_and_head():
+    M, ffn = 9, 1024
+    gu0 = rnd_bits((M, 2 * ffn), 8, 3.0)
+    act = torch.empty(M, ffn, dtype=torch.int16, device=DEV)
+    dyq.silu_mul(t16(gu0), M, ffn, act)
+    g = glue.from_bf16_bits(gu0)
+    close_bf16(f64(act), glue.silu_mul(g[:, :ffn], g[:, ffn:]))
+    E, d, nb, stride = 3, 512, 256, 5
+    x0 = rnd_bits((E * stride, d), 9)
+    W0 = rnd_bits((nb, d), 10, 0.5)
+    logits = torch.empty(E, nb, dtype=torch.float32, device=DEV)
+    tok = torch.full((E * 7,), -1, dtype=torch.int32, device=DEV)
+    dyq.head_argmax(t16(x0), E, stride, d, t16(W0), nb, logits, tok[2:], 7)
+    xr = glue.from_bf16_bits(x0)[::stride]
+    lg, am = glue.head_argmax(xr, glue.from_bf16_bits(W0))
+    assert np.allclose(logits.cpu().numpy(), lg, rtol=1e-4, atol=1e-3)
+    assert np.array_equal(tok.cpu().numpy()[2::7][:E], am)
+
+
+# ------------------------------------------------------------------ whole step
+def _tiny(seed=0):
+    rng = np.random.default_rng(seed)
+    L, d, ffn, V, nb = 2, 256, 512, 512, 256
+    shapes = [(3 * d, d), (d, d), (2 * ffn, d), (d, ffn)]
+    w = {"lin": [[synth.weights_bf16(N, K, seed=100 * l + i + seed) for i, (N, K) in enumerate(shapes)]
+                 for l in range(L)],
+         "attn_norm": glue.to_bf16_bits(1 + 0.1 * rng.standard_normal((L, d))),
+         "mlp_norm": glue.to_bf16_bits(1 + 0.1 * rng.standard_normal((L, d))),
+         "final_norm": glue.to_bf16_bits(1 + 0.1 * rng.standard_normal(d)),
+         "embed": glue.to_bf16_bits(rng.standard_normal((V, d))),
+         "head": glue.to_bf16_bits(rng.standard_normal((nb, d)))}
+    return w
+
+
+def _gpu_model(w, E, n_vis, n_text):
+    layers = [[dyq.PackedLinear.from_bf16(t16(lin), group=64, wbits=4) for lin in layer] for layer in w["lin"]]
+    return dyq.Model(layers, t16(w["attn_norm"]), t16(w["mlp_norm"]), t16(w["final_norm"]), t16(w["embed"]),
+                     t16(w["head"]), E=E, n_heads=2, n_vis=n_vis, n_text=n_text, n_act=7)
+
+
+def _margins(logits):
+    s = np.sort(logits, axis=-1)
+    return s[:, -1] - s[:, -2]
+
+
+def test_policy_step_matches_reference_and_selector():
+    E, n_vis, n_text = 2, 8, 4
+    w = _tiny()
+    model = _gpu_model(w, E, n_vis, n_text)
+    ref = glue.TinyModel(w, 64, 4, 2, n_vis, n_text, 7)
+    cal = dyq.default_calib()
+    state = torch.zeros(dyq.state_size(E, cal), dtype=torch.uint8, device=DEV)
+    dyq.state_init(E, cal, state)
+    sel = oracle.SelectState(E)
+    rng = np.random.default_rng(11)
+    act = torch.zeros(E, 7, dtype=torch.float32, device=DEV)
+    bits = torch.zeros(E, dtype=torch.int32, device=DEV)
+    prev = None
+    exact = total = 0
+    for step in range(14):
+        vis = glue.to_bf16_bits(rng.standard_normal((E, n_vis, 256)))
+        text = rng.integers(0, 256, (E, n_text)).astype(np.int32)
+        model.step(state, E, t16(vis.reshape(E, -1)), torch.from_numpy(text).to(DEV), act, bits)
+        a = act.cpu().numpy()
+        b = bits.cpu().numpy()
+        # b*_t: bit-exact with the oracle selector fed the GPU's own previous actions
+        rb = sel.step(prev)["bits"]
+        assert np.array_equal(b, rb), (step, b, rb)
+        prev = a.astype(np.float32)
+        assert np.all(np.abs(a) < 1.0)
+        for e in range(E):
+            gtok = np.rint((a[e] + 1.0) * 128.0 - 0.5).astype(int)   # detok^-1 (256 bins)
+            assert np.array_equal(glue.detok(gtok, 256), a[e])
+            _, logits = ref.episode(vis[e], text[e], int(b[e]), forced=gtok)
+            # teacher-forced: every GPU decision is the reference argmax, or within
+            # bf16-glue noise of it (a quantization code may flip on a boundary)
+            top = logits.max(axis=1)
+            tol = 5e-3 * np.abs(logits).max()
+            assert np.all(logits[np.arange(7), gtok] >= top - tol), (step, e, gtok, logits.argmax(1))
+            exact += int((logits.argmax(axis=1) == gtok).sum())
+            total += 7
+    assert exact >= 0.9 * total, (exact, total)
+
+
+def test_policy_step_repeat_is_deterministic():
+    E, n_vis, n_text = 3, 8, 4
+    w = _tiny(1)
+    model = _gpu_model(w, E, n_vis, n_text)
+    cal = dyq.default_calib()
+    outs = []
+    for _ in range(2):
+        model.init()
+        state = torch.zeros(dyq.state_size(E, cal), dtype=torch.uint8, device=DEV)
+        dyq.state_init(E, cal, state)
+        rng = np.random.default_rng(12)
+        act = torch.zeros(E, 7, dtype=torch.float32, device=DEV)
+        seq = []
+        for _ in range(12):
+            vis = t16(glue.to_bf16_bits(rng.standard_normal((E, n_vis * 256))))
+            text = torch.from_numpy(rng.integers(0, 256, (E, n_text)).astype(np.int32)).to(DEV)
+            model.step(state, E, vis, text, act)
+            seq.append(act.cpu().numpy().copy())
+        outs.append(np.array(seq))
+    assert np.array_equal(outs[0], outs[1])
