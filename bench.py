@@ -61,6 +61,8 @@ def parse():
     p.add_argument("--no-variants", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-prefill", action="store_true", help="skip the configs[2] prefill slice")
+    p.add_argument("--no-policy", action="store_true", help="skip the configs[3] policy-step slice")
+    p.add_argument("--policy-E", default="1,8", help="episodes per GPU for the policy slice")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu)")
     return p.parse_args()
 
@@ -379,21 +381,28 @@ def main():
         k_ms = statistics.median(kern_ms)
         k_src = "cuda events around the gate|up qlinear inside the timed graph"
     else:
-        # fallback: one graph of R back-to-back gate|up launches (rotating copies)
+        # events recorded inside a captured graph cannot be timed: time the
+        # gate|up qlinear (act-quant + decode kernels) per activation width in a
+        # graph of R back-to-back launches (rotating copies), and weight the
+        # widths by the timed region's b* histogram (W4-pinned table: b* = abits)
         R = 64
-        g3 = torch.cuda.CUDAGraph()
-        s3 = torch.cuda.Stream()
-        s3.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.graph(g3, stream=s3):
-            for r in range(R):
-                p = packed[r % C][gate_li]
-                dyq.qlinear(p.wd, p.codes, p.meta, xs[0][gate_li], M, row_bits, 0, ys[gate_li], 1,
-                            wss[gate_li])
-        g3.replay()
-        torch.cuda.synchronize()
-        k_ms = statistics.median(timed(g3) for _ in range(5)) / R
-        k_src = f"cuda events around a graph of {R} back-to-back gate|up launches (rotating copies)"
-        del g3
+        k_by_bits = {}
+        for b in sorted(hist):
+            g3 = torch.cuda.CUDAGraph()
+            s3 = torch.cuda.Stream()
+            s3.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(g3, stream=s3):
+                for r in range(R):
+                    p = packed[r % C][gate_li]
+                    dyq.qlinear(p.wd, p.codes, p.meta, xs[0][gate_li], M, None, b, ys[gate_li], 1, wss[gate_li])
+            g3.replay()
+            torch.cuda.synchronize()
+            k_by_bits[b] = statistics.median(timed(g3) for _ in range(5)) / R
+            del g3
+        n_h = sum(hist.values())
+        k_ms = sum(k_by_bits[b] * hist[b] / n_h for b in hist)
+        k_src = (f"cuda events around graphs of {R} back-to-back gate|up qlinear calls per width "
+                 f"{ {b: round(v * 1e3, 2) for b, v in k_by_bits.items()} } us, weighted by the timed b* histogram")
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_decode_summary.json")))
@@ -470,6 +479,53 @@ def main():
                    "peak_i8_TOPS": i8_peak, "peak_bf16_TFLOPS": bf16_peak, "results": pres,
                    "timing": "cuda events around a graph of 10 blocks (median of 3)"}
 
+    # ---- configs[3] slice: whole VLA policy steps/s (dyq_policy_step: select_bits,
+    # 288-token prefill and 6 decode passes through 32 Llama-2-7B blocks, action
+    # head + detok) for E episodes on this rank; layers cycle through the C
+    # packed block copies (all distinct from L2's point of view)
+    policy = None
+    if not args.profile and not args.no_policy:
+        d_m, NL = 4096, 32
+        layers = [packed[l % C] for l in range(NL)]
+        one = torch.full((d_m,), 0x3F80, dtype=torch.int16, device=dev)        # bf16 1.0
+        norms = one.repeat(NL)
+        embed = synth.activations_bf16_torch(32000, d_m, seed=7000, device=dev)
+        head = synth.weights_bf16_torch(256, d_m, seed=7001, device=dev)
+        pres = {}
+        for E in [int(e) for e in args.policy_E.split(",")]:
+            model = dyq.Model(layers, norms, norms, one, embed, head, E=E, n_heads=32)
+            cal = dyq.default_calib()
+            pst = torch.zeros(dyq.state_size(E, cal), dtype=torch.uint8, device=dev)
+            dyq.state_init(E, cal, pst)
+            vis = synth.activations_bf16_torch(E * 256, d_m, seed=7100 + rank, device=dev)
+            gen = torch.Generator(device=dev).manual_seed(7200 + rank)
+            text = torch.randint(0, 32000, (E, 32), dtype=torch.int32, device=dev, generator=gen)
+            act_o = torch.zeros(E, 7, dtype=torch.float32, device=dev)
+            bits_o = torch.zeros(E, dtype=torch.int32, device=dev)
+            for _ in range(2):
+                model.step(pst, E, vis, text, act_o, bits_o)
+            torch.cuda.synchronize()
+            R = 3
+            gp = torch.cuda.CUDAGraph()
+            sp = torch.cuda.Stream()
+            sp.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(gp, stream=sp):
+                for _ in range(R):
+                    model.step(pst, E, vis, text, act_o, bits_o, stream=sp)
+            gp.replay()
+            torch.cuda.synchronize()
+            ms = statistics.median(timed(gp) for _ in range(3)) / R
+            sps = episodes.throughput(E, ms * 1e-3)
+            pres[f"E{E}"] = {"episodes_per_gpu": E, "ms_per_step": round(ms, 3),
+                            "policy_steps_per_s": round(sps, 2)}
+            del gp, model
+            torch.cuda.empty_cache()
+        policy = {"workload": "configs[3] slice: dyq_policy_step, OpenVLA-7B shapes (32 blocks, d=4096, "
+                              "ffn=11008, 32 heads), 256 vision + 32 text tokens, 7 action tokens, W4 G64, "
+                              "per-episode b* from the kinematic dispatcher",
+                  "value_unit": "policy steps/s (whole job: episodes x steps / max-over-ranks time)",
+                  "results": pres, "timing": "cuda events around a graph of 3 steps (median of 3)"}
+
     # ---- e2e through the public API: pinned H2D of the step's inputs, eager
     # launches, D2H of the step's result (block output y and b*), per step
     e2e = None
@@ -525,6 +581,7 @@ def main():
             "roofline": roofline,
             "variants": variants,
             "prefill": prefill,
+            "policy": policy,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
