@@ -288,6 +288,28 @@ DYQ_API dyq_status_t dyq_head_argmax(const uint16_t* x, int32_t E, int32_t row_s
                                      const uint16_t* head_bins, int32_t n_bins, float* logits, int32_t* tok,
                                      int32_t tok_stride, dyq_stream_t stream);
 
+/* ====================================================== tensor parallelism
+ * SURVEY.md §8(a) A8 / BASELINE config 5 (not in the paper): column (N)
+ * sharding of every quantized linear across the GPUs of one node.  Rank r packs
+ * rows [n0, n1) = dyq_tp_shard(N, P, r) of the weight (K-groups never span
+ * ranks, so the shard's pack equals the row slice of the full pack), runs
+ * dyq_qlinear into y_shard [M, N/P] bf16, and dyq_tp_allgather joins the shards
+ * with an NCCL all-gather over NVLink (NCCL is dlopen'ed: libnccl.so.2, or the
+ * path in $DYQ_NCCL_LIB) plus a column interleave. */
+DYQ_API dyq_status_t dyq_tp_shard(int32_t N, int32_t world, int32_t rank, int32_t* n0, int32_t* n1);
+/* id_host: host buffer of 128 bytes (ncclUniqueId), created on one rank and
+ * broadcast by the caller (e.g. over the torch process group). */
+DYQ_API dyq_status_t dyq_comm_unique_id(void* id_host);
+DYQ_API dyq_status_t dyq_comm_init(const void* id_host, int32_t rank, int32_t world, void** comm);
+DYQ_API dyq_status_t dyq_comm_destroy(void* comm);
+/* y [M, N] bf16 (every rank) <- concat_r y_shard_r [M, N/P]; gather_buf device
+ * [P, M, N/P] bf16 (unused, may be NULL, when M == 1).  N % (16 P) == 0. */
+DYQ_API dyq_status_t dyq_tp_allgather(void* comm, const uint16_t* y_shard, int32_t M, int32_t N,
+                                      uint16_t* gather_buf, uint16_t* y, dyq_stream_t stream);
+/* the interleave step alone: y[m, r Ns + j] = buf[r, m, j] (Ns % 8 == 0) */
+DYQ_API dyq_status_t dyq_tp_interleave(const uint16_t* buf, int32_t P, int32_t M, int32_t Ns, uint16_t* y,
+                                       dyq_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
     _drain(procs)
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-                           "-Xcompiler", "-fPIC", "-o", tmp, *objs])
+                           "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

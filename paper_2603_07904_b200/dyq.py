@@ -50,6 +50,12 @@ _SIGS = {
     "dyq_attention_decode": [P, i32, i32, i32, i32, P, i32, i32, i32, P, P],
     "dyq_silu_mul": [P, i32, i32, P, P],
     "dyq_head_argmax": [P, i32, i32, i32, P, i32, P, P, i32, P],
+    "dyq_tp_shard": [i32, i32, i32, P, P],
+    "dyq_comm_unique_id": [P],
+    "dyq_comm_init": [P, i32, i32, P],
+    "dyq_comm_destroy": [P],
+    "dyq_tp_allgather": [P, P, i32, i32, P, P, P],
+    "dyq_tp_interleave": [P, i32, i32, i32, P, P],
 }
 _RESTYPES = {"dyq_last_error": C.c_char_p, "dyq_version": C.c_char_p}
 
@@ -357,3 +363,44 @@ class Model:
             except Exception:
                 pass
             self._h = None
+
+
+# ------------------------------------------------------ tensor parallelism
+def tp_shard(N: int, world: int, rank: int) -> tuple[int, int]:
+    a, b = C.c_int32(0), C.c_int32(0)
+    _call("dyq_tp_shard", N, world, rank, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _call("dyq_comm_unique_id", buf)
+    return buf.raw
+
+
+class Comm:
+    """NCCL communicator of libdyq.so (column-sharded TP)."""
+
+    def __init__(self, unique_id: bytes, rank: int, world: int):
+        self.rank, self.world = rank, world
+        self._id = C.create_string_buffer(unique_id, 128)
+        self._h = C.c_void_p()
+        _call("dyq_comm_init", self._id, rank, world, C.byref(self._h))
+
+    def allgather(self, y_shard, M: int, N: int, gather_buf, y, stream=None):
+        _call("dyq_tp_allgather", self._h, _ptr(y_shard), M, N, _ptr(gather_buf), _ptr(y), _stream(stream))
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().dyq_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def tp_interleave(buf, P: int, M: int, Ns: int, y, stream=None):
+    _call("dyq_tp_interleave", _ptr(buf), P, M, Ns, _ptr(y), _stream(stream))
