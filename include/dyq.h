@@ -67,6 +67,12 @@ typedef enum {
 DYQ_API const char* dyq_last_error(void);
 /* Library version string, e.g. "dyq 0.1 sm_100a". */
 DYQ_API const char* dyq_version(void);
+/* Debug/profiling only: record %globaltimer events of the decode-path kernels
+ * into a caller-owned DEVICE buffer laid out as [u64 count][u64 capacity]
+ * [capacity x {u64 tag, u64 ns}], tag = serial << 32 | kernel << 24 |
+ * event << 16 | blockIdx.x.  dev_buf = NULL disables (the default).  The header
+ * words are written with an async copy on `stream`.  DYQ_EINVAL if bytes < 64. */
+DYQ_API dyq_status_t dyq_trace_enable(void* dev_buf, int64_t bytes, dyq_stream_t stream);
 
 /* ---------------------------------------------------------------- errors */
 /* err: device int64; reset to INT64_MAX (= no error). */
@@ -198,6 +204,15 @@ DYQ_API dyq_status_t dyq_qlinear_q(const dyq_wdesc_t* wd, const void* codes, con
                                    const uint16_t* x, int32_t M, const int32_t* row_bits,
                                    int32_t bits, void* y, int32_t y_dtype, void* workspace,
                                    size_t ws_bytes, dyq_stream_t stream);
+
+/* Asynchronous HBM -> L2 prefetch of `bytes` bytes at device address p
+ * (16-byte aligned), e.g. the next layer's packed codes and metadata, issued
+ * while the current layer's dependent chain (act-quant -> qlinear) runs.  The
+ * packed weights never depend on earlier kernels (weights are frozen),
+ * so the transfer overlaps that chain; stream-ordered, no host sync.  A hint
+ * only: results never depend on it.  Bytes beyond the L2 capacity (126 MB on
+ * B200) evict earlier prefetched lines.  DYQ_EINVAL on a null / misaligned p. */
+DYQ_API dyq_status_t dyq_prefetch_l2(const void* p, size_t bytes, dyq_stream_t stream);
 
 /* Test hook: same main loop, writes the exact integer group sums
  * I[m,n,g] (int32 [M,N,K/G]; 0 for A16 rows) instead of y. */

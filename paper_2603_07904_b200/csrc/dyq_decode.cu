@@ -9,25 +9,30 @@
 //
 //  * work unit = (128-row tile, K-group); a pipeline STAGE = up to GPS
 //    consecutive units of one tile (~16 KB of codes: one bulk copy) + their
-//    metadata (one copy) + the activation slices (one copy per array) -- big
-//    copies keep the TMA engine's per-copy cost off the critical path;
-//  * one CTA per SM (stream-K: contiguous unit ranges, tile-major); the
-//    producer issues the first stages' WEIGHT copies before griddepcontrol.wait,
-//    so weight streaming starts under programmatic dependent launch (PDL);
-//  * one producer thread runs an S-stage mbarrier ring (cp.async.bulk);
-//  * 16 consumer warps, warp w = 16-row sub-tile w & 7, working on every group
-//    of the stages of parity w >> 3: one LDS.128 per lane is the
+//    metadata (one copy) + the activation records of those K-groups (one copy,
+//    plus one for the bf16 rows of BF16-bypass tokens) -- big copies keep the
+//    TMA engine's per-copy cost off the critical path;
+//  * stream-K: contiguous unit ranges, tile-major, one CTA per SM; 8 consumer
+//    warps (warp w = 16-row sub-tile w) + 1 producer warp, <= 113 KB of shared
+//    memory and <= 112 registers per thread so that TWO CTAs fit on an SM: under
+//    programmatic dependent launch (PDL) the next layer's CTAs become resident
+//    while this layer drains and stream their weights into their own ring
+//    (issued before griddepcontrol.wait -- weights never depend on the previous
+//    kernel), hiding the per-call dependency latency (act-quant -> MMA);
+//  * consumer math per (sub-tile, group): one LDS.128 per lane is the
 //    exact register image of two mma.m16n8k32 A fragments (pre-permuted by
 //    dyq_pack_weights); nibbles widen with LOP3s; integer tokens run
 //    IMMA.16832.U8.U8 (tokens = the n8 dimension) with the exact per-group
 //    zero-point algebra
 //        I = P - z_w*SX - z_x*(Sum q - G*z_w),   P = Sum Xq*q   (int32)
 //    where Sum q comes from one more IMMA against an all-ones B (no shuffles);
+//    A2/A4-only calls use centred s8 codes (I = P' - z_w*SXc, one IMMA);
 //    A16 tokens (the BF16 bypass) convert the same registers to bf16
 //    (q - z_w is exact) and run HMMA.16816 against x;
 //  * y = Sum_g s_x s_w I in fp32 (packed FMUL2/FFMA2); a tile split across
-//    CTAs is reduced deterministically: each contributor writes a private
-//    slot, the last to arrive (per-tile counter) sums slots in slot order.
+//    CTAs is reduced per WARP (no CTA barrier): each contributor writes a
+//    private slot, the last to arrive on the (tile, sub-tile) counter sums the
+//    slots in contributor order (deterministic) and writes y.
 #include <stdlib.h>
 
 #include "dyq_internal.cuh"
@@ -46,15 +51,16 @@ struct DecArgs {
     void* y;                // base [Mtotal, N]
     int y_dtype;
     int32_t* I_out;         // base [Mtotal, N, NG] (partials mode)
-    const uint8_t* ws;      // activation workspace (ActLayoutDec)
+    const uint8_t* ws;      // activation area (ActLayoutDec)
     ActLayoutDec A;
     float* part;            // split-K slots [(grid + T128)][16 tok][128 rows]
-    int* counters;          // [T128]
+    int* counters;          // [T128][8 sub-tiles]
     int upc;                // units per CTA
     int gps;                // groups (units) per stage
     int stages, stage_bytes;
-    int off_meta, off_par, off_xq, off_x16;  // offsets inside a stage
-    int debug_skip;         // DYQ_DEBUG_SKIP=1: consumers skip the math (copy-path timing only; debug)
+    int off_meta, off_cp, off_x16;  // offsets inside a stage
+    uint64_t* trace;                // dyq_trace_enable buffer or null
+    uint32_t serial;
 };
 
 __device__ __forceinline__ void mma_u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -119,78 +125,133 @@ __device__ __forceinline__ uint32_t u8pair_to_bf16(uint32_t v, int hi_pair, uint
     }
 }
 
-constexpr int DEC_CWARPS = 16;  // consumer warps: (sub-tile w & 7) x (stage parity w >> 3)
+#ifndef DYQ_DEC_CWARPS
+#define DYQ_DEC_CWARPS 16
+#endif
+#ifndef DYQ_DEC_UNROLL
+#define DYQ_DEC_UNROLL 2
+#endif
+// consumer warps: warp w = sub-tile w & 7; with 16 warps, warp w >> 3 takes the
+// odd / even groups of every stage and the pair combines through shared memory
+constexpr int DEC_CWARPS = DYQ_DEC_CWARPS;
 constexpr int DEC_THREADS = 32 * (DEC_CWARPS + 1);  // + 1 producer warp
-constexpr int DEC_CONSUMERS = 32 * DEC_CWARPS;
+constexpr int DEC_UNROLL = DYQ_DEC_UNROLL;
+constexpr int DEC_MINB = DEC_CWARPS == 8 ? 2 : 1;   // CTAs per SM (register budget)
 
 enum { MODE_INT = 0, MODE_A16 = 1, MODE_MIXED = 2, MODE_INTC = 3 };  // INTC: centred s8 activation codes
 
-// Split-K tile flush: direct store when the CTA owns the whole tile, otherwise
-// private slot + last-arriver deterministic reduction.
+// Per-warp scratch for split-K slot publication (after the stages and the
+// 16-warp combine area).
+__device__ __forceinline__ float* dec_slot_scratch(const DecArgs& a, int sub) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    return reinterpret_cast<float*>(smem + 256 + (size_t)a.stages * a.stage_bytes + 8 * 32 * 8 * 4) + sub * 256;
+}
+// Lane 0 of a contributor warp: once its bulk slot store completed, count it.
+__device__ __forceinline__ void dec_publish(int*& pend, int lane) {
+    if (lane == 0 && pend) {
+        ptx::bulk_wait_all();
+        ptx::red_add_relaxed_gpu(pend, 1);
+        pend = nullptr;
+    }
+}
+
+// Split-K flush of one sub-tile by its warp.  When the CTA owns the whole
+// tile: direct store.  Otherwise the contributors of a tile are the CTAs
+// c_first..c_last of the stream-K order; CTA c_first holds the tile's FIRST
+// groups at the END of its range, every other contributor holds its part at
+// the START of its range.  So c_first is the designated reducer: the others
+// write a private slot and release-increment the (tile, sub-tile) counter
+// without waiting (fire and forget, long before c_first gets there); c_first
+// acquires the counter, adds the slots in contributor order (deterministic)
+// to its own partial sums and writes y.  All CTAs of the grid are co-resident
+// (grid <= #SMs, one CTA per SM), so the reducer's wait always ends.
 template <int NT8>
-__device__ __forceinline__ void dec_flush(const DecArgs& a, int tile, const float (&facc)[NT8][4], int warp,
-                                          int gid, int t, int* s_flag) {
+__device__ __forceinline__ void dec_flush_warp(const DecArgs& a, int tile, const float (&facc)[NT8][4], int sub,
+                                               int lane, int*& pend) {
     const WLayout& L = a.L;
     const int NG = L.NG;
     const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
-    const int nrows = nsub * 16;
+    if (sub >= nsub) return;  // warp-uniform
+    const int gid = lane >> 2, t = lane & 3;
     const int c_first = (tile * NG) / a.upc;
     const int c_last = (tile * NG + NG - 1) / a.upc;
     const int nc = c_last - c_first + 1;
-    if (nc == 1) {
-        if (warp < nsub) {
-#pragma unroll
-            for (int j = 0; j < NT8; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int tok = j * 8 + 2 * t + (i & 1);
-                    if (tok < a.M) {
-                        const size_t o = (size_t)(a.m0 + tok) * L.N + tile * 128 + warp * 16 + gid + 8 * (i >> 1);
-                        if (a.y_dtype == 0)
-                            reinterpret_cast<float*>(a.y)[o] = facc[j][i];
-                        else
-                            reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(facc[j][i]);
-                    }
-                }
-        }
-        return;
-    }
+    const int c = (int)blockIdx.x - c_first;
+    auto store = [&](int tok, int r, float v) {
+        const size_t o = (size_t)(a.m0 + tok) * L.N + tile * 128 + sub * 16 + r;
+        if (a.y_dtype == 0)
+            reinterpret_cast<float*>(a.y)[o] = v;
+        else
+            reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(v);
+    };
+    int* cnt = &a.counters[tile * 8 + sub];
     const int base = c_first + tile;  // slot range of this tile
-    float* P = a.part + (size_t)(base + ((int)blockIdx.x - c_first)) * 16 * 128;
-    if (warp < nsub) {
+    if (nc > 1 && c != 0) {
+        // slot = [sub][16 tok][16 rows] fp32, published through the async proxy
+        // (bulk store): the relaxed counter increment follows the completion of
+        // the copy (cp.async.bulk.wait_group), deferred to the next stage
+        // boundary (dec_publish) so this warp never stalls on it.  No
+        // gpu-scope release fence (MEMBAR.ALL.GPU would wait for the CTA's
+        // in-flight weight copies).
+        float* scr = dec_slot_scratch(a, sub);
 #pragma unroll
         for (int j = 0; j < NT8; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int tok = j * 8 + 2 * t + (i & 1);
-                P[tok * 128 + warp * 16 + gid + 8 * (i >> 1)] = facc[j][i];
-            }
-    }
-    ptx::named_bar_sync(1, DEC_CONSUMERS);
-    if (threadIdx.x == 0) *s_flag = (ptx::atom_add_acq_rel_gpu(&a.counters[tile], 1) == nc - 1);
-    ptx::named_bar_sync(1, DEC_CONSUMERS);
-    if (*s_flag) {
-        for (int idx = threadIdx.x; idx < a.M * nrows; idx += DEC_CONSUMERS) {
-            const int tok = idx / nrows, r = idx - tok * nrows;
-            // all slot loads in flight before the (slot-ordered, deterministic) sum
-            const float* src = a.part + (size_t)base * 16 * 128 + tok * 128 + r;
-            float sum = 0.f;
-            for (int k0 = 0; k0 < nc; k0 += 16) {
-                float v[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) v[k] = (k0 + k < nc) ? __ldcg(src + (size_t)(k0 + k) * 16 * 128) : 0.f;
-#pragma unroll
-                for (int k = 0; k < 16; ++k) sum += v[k];
-            }
-            const size_t o = (size_t)(a.m0 + tok) * L.N + tile * 128 + r;
-            if (a.y_dtype == 0)
-                reinterpret_cast<float*>(a.y)[o] = sum;
-            else
-                reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(sum);
+            for (int i = 0; i < 4; ++i) scr[(j * 8 + 2 * t + (i & 1)) * 16 + gid + 8 * (i >> 1)] = facc[j][i];
+        ptx::fence_proxy_async_cta();
+        __syncwarp();
+        if (lane == 0) {
+            ptx::bulk_wait_all();  // previous publication of this warp (scratch reuse)
+            if (pend) ptx::red_add_relaxed_gpu(pend, 1);
+            float* P = a.part + ((size_t)(base + c) * 8 + sub) * 16 * 16;
+            ptx::bulk_s2g(P, ptx::smem_u32(scr), NT8 * 8 * 16 * 4);
+            pend = cnt;
         }
-        if (threadIdx.x == 0) a.counters[tile] = 0;  // self-cleaning for the next call
+        return;
     }
-    ptx::named_bar_sync(1, DEC_CONSUMERS);
+    float v[NT8][4];
+#pragma unroll
+    for (int j = 0; j < NT8; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[j][i] = facc[j][i];
+    if (nc > 1) {
+        if (lane == 0) {
+            if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 1, 5);
+            while (ptx::ld_acquire_gpu(cnt) < nc - 1) __nanosleep(64);
+            if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 1, 6);
+            *cnt = 0;  // self-cleaning: the next call's contributors start after this kernel
+        }
+        __syncwarp();
+        const float* src = a.part + ((size_t)base * 8 + sub) * 16 * 16;
+        constexpr int SL = 8 * 16 * 16;  // floats per slot
+        // all slots' loads in flight at once (one L2 round trip per 8 contributors),
+        // then the sums in contributor order
+        for (int c0 = 1; c0 < nc; c0 += 8) {
+            float w[8][NT8][4];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+#pragma unroll
+                for (int j = 0; j < NT8; ++j)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        w[k][j][i] = (c0 + k < nc) ? __ldcg(src + (c0 + k) * SL + (j * 8 + 2 * t + (i & 1)) * 16 +
+                                                            gid + 8 * (i >> 1))
+                                                   : 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+#pragma unroll
+                for (int j = 0; j < NT8; ++j)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) v[j][i] += w[k][j][i];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NT8; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int tok = j * 8 + 2 * t + (i & 1);
+            if (tok < a.M) store(tok, gid + 8 * (i >> 1), v[j][i]);
+        }
 }
 
 // One group (unit) of one 16-row sub-tile for this warp.  `st` = stage base
@@ -199,11 +260,13 @@ template <int WBITS, int NT8, int SPG, int MODE, bool PARTIALS>
 __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi, int g, int tile, int nsub,
                                           float (&facc)[NT8][4], uint32_t is16_mask) {
     constexpr int G = SPG * 64;
+    constexpr int CPS = NT8 * 8 * G + NT8 * 64;  // activation record bytes per group (ActLayoutDec::cp_stride)
+    constexpr int X16S = NT8 * 8 * G * 2;        // bf16 rows per group (ActLayoutDec::x16_stride)
     const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & 7;  // warp = sub-tile
     const int gid = lane >> 2, t = lane & 3;
     const WLayout& L = a.L;
     const uint32_t ONES = 0x01010101u;
-    const int gps = a.gps;
+    const uint32_t rec = st + a.off_cp + gi * CPS;
     const uint32_t mb = st + a.off_meta + gi * META_BLOCK;
     const uint2 swr2 = ptx::lds64(mb + meta_slot(warp, gid) * 4);
     const float sw0 = __uint_as_float(swr2.x), sw1 = __uint_as_float(swr2.y);
@@ -250,7 +313,7 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
             // centred s8 activations: P' = Sum q (Xq - z_x) directly
 #pragma unroll
             for (int j = 0; j < NT8; ++j) {
-                const uint4 xb = ptx::lds128(st + a.off_xq + ((j * gps + gi) * 8 + gid) * G + spi * 64 + t * 16);
+                const uint4 xb = ptx::lds128(rec + (j * 8 + gid) * G + spi * 64 + t * 16);
                 mma_u8s8(iacc[j], A[0], xb.x, xb.y);
                 mma_u8s8(iacc[j], A[1], xb.z, xb.w);
             }
@@ -260,7 +323,7 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
             mma_u8(sq, A[1], ONES, ONES);
 #pragma unroll
             for (int j = 0; j < NT8; ++j) {
-                const uint4 xb = ptx::lds128(st + a.off_xq + ((j * gps + gi) * 8 + gid) * G + spi * 64 + t * 16);
+                const uint4 xb = ptx::lds128(rec + (j * 8 + gid) * G + spi * 64 + t * 16);
                 mma_u8(iacc[j], A[0], xb.x, xb.y);
                 mma_u8(iacc[j], A[1], xb.z, xb.w);
             }
@@ -268,7 +331,7 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
         if (MODE == MODE_A16 || MODE == MODE_MIXED) {
 #pragma unroll
             for (int j = 0; j < NT8; ++j) {
-                const uint32_t xr = st + a.off_x16 + (((j * gps + gi) * 8 + gid) * G + spi * 64 + t * 16) * 2;
+                const uint32_t xr = st + a.off_x16 + gi * X16S + ((j * 8 + gid) * G + spi * 64 + t * 16) * 2;
                 const uint4 xa = ptx::lds128(xr);       // slab 0: h0 (x,y), h1 (z,w)
                 const uint4 xc = ptx::lds128(xr + 16);  // slab 1
 #pragma unroll
@@ -294,7 +357,7 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
 #pragma unroll
     for (int j = 0; j < NT8; ++j) {
         uint4 pp = make_uint4(0u, 0u, 0u, 0u);
-        if (MODE != MODE_A16) pp = ptx::lds128(st + a.off_par + gi * 128 + (j * 8 + 2 * t) * 8);
+        if (MODE != MODE_A16) pp = ptx::lds128(rec + NT8 * 8 * G + (j * 8 + 2 * t) * 8);
         const float sx0 = __uint_as_float(pp.x), sx1 = __uint_as_float(pp.z);
         const int zx0 = (int)(pp.y >> 16), zx1 = (int)(pp.w >> 16);
         const int SX0 = (int)(pp.y & 0xffffu), SX1 = (int)(pp.w & 0xffffu);
@@ -345,43 +408,49 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
     }
 }
 
-// Consumer loop over the CTA's stages (must enumerate stages exactly like the
-// producer).  Consumer warp w works on sub-tile w & 7 for every group of the
-// stages of parity w >> 3; the two parities' partial sums are combined through
-// shared memory only when a tile is flushed.
+// End of this CTA's part of a tile: with 16 consumer warps the odd-group warp
+// of each sub-tile hands its partial sums to the even-group warp (shared
+// memory + a 64-thread named barrier per sub-tile), which flushes.
 template <int NT8>
-__device__ __forceinline__ void combine_parities(float (&facc)[NT8][4], float* scr, int par, int sub, int lane) {
-    float* p = scr + (sub * 32 + lane) * (NT8 * 4);
-    if (par == 1) {
+__device__ __forceinline__ void dec_tile_done(const DecArgs& a, int tile, float (&facc)[NT8][4], int sub, int par,
+                                              int lane, int*& pend) {
+    if constexpr (DEC_CWARPS == 16) {
+        extern __shared__ __align__(128) uint8_t smem[];
+        float* p = reinterpret_cast<float*>(smem + 256 + (size_t)a.stages * a.stage_bytes) + (sub * 32 + lane) * 8;
+        if (par == 1) {
 #pragma unroll
-        for (int j = 0; j < NT8; ++j)
+            for (int j = 0; j < NT8; ++j)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) p[j * 4 + k] = facc[j][k];
+                for (int k = 0; k < 4; ++k) p[j * 4 + k] = facc[j][k];
+        }
+        ptx::named_bar_sync(1 + sub, 64);
+        if (par == 0) {
+#pragma unroll
+            for (int j = 0; j < NT8; ++j)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) facc[j][k] += p[j * 4 + k];
+        }
+        ptx::named_bar_sync(1 + sub, 64);
+        if (par == 1) return;
     }
-    ptx::named_bar_sync(2, DEC_CONSUMERS);
-    if (par == 0) {
-#pragma unroll
-        for (int j = 0; j < NT8; ++j)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) facc[j][k] += p[j * 4 + k];
-    }
-    ptx::named_bar_sync(2, DEC_CONSUMERS);
+    dec_flush_warp<NT8>(a, tile, facc, sub, lane, pend);
 }
 
+// Consumer loop over the CTA's stages (must enumerate stages exactly like the
+// producer).  Consumer warp w works on sub-tile w for every group.
 template <int WBITS, int NT8, int SPG, int MODE, bool PARTIALS>
 __device__ __forceinline__ void dec_consume(const DecArgs& a, uint32_t bar_full, uint32_t bar_empty,
-                                            uint32_t stage0, int* s_flag, float* scr, int u0, int u1,
-                                            uint32_t is16_mask) {
+                                            uint32_t stage0, int u0, int u1, uint32_t is16_mask) {
     const WLayout& L = a.L;
     const int NG = L.NG;
     const int S = a.stages;
-    const int lane = threadIdx.x & 31, cw = threadIdx.x >> 5;
-    const int sub = cw & 7, par = cw >> 3;
-    const int gid = lane >> 2, t = lane & 3;
+    const int lane = threadIdx.x & 31, sub = (threadIdx.x >> 5) & 7, par = threadIdx.x >> 8;
+    constexpr int GSTEP = DEC_CWARPS / 8;
     const uint32_t stage_bytes = (uint32_t)a.stage_bytes;
-    int s = 0, i = 0;
+    int s = 0;
     uint32_t ph = 0;
     int cur_tile = -1;
+    int* pend = nullptr;  // lane 0: counter to bump once the published slot landed
     float facc[NT8][4];
 #pragma unroll
     for (int j = 0; j < NT8; ++j)
@@ -389,57 +458,54 @@ __device__ __forceinline__ void dec_consume(const DecArgs& a, uint32_t bar_full,
         for (int k = 0; k < 4; ++k) facc[j][k] = 0.f;
     const int gps = a.gps;
     int tile = u0 / NG, g0 = u0 - (u0 / NG) * NG;  // one division per CTA, then incremental
-    for (int u = u0; u < u1; ++i) {
+    for (int u = u0; u < u1;) {
         if (g0 == NG) { g0 = 0; ++tile; }
         int n = NG - g0;
         n = n < gps ? n : gps;
         n = n < u1 - u ? n : u1 - u;
         if (!PARTIALS && tile != cur_tile) {
-            if (cur_tile >= 0) {
-                combine_parities<NT8>(facc, scr, par, sub, lane);
-                dec_flush<NT8>(a, cur_tile, facc, par ? 8 : sub, gid, t, s_flag);
-            }
+            if (cur_tile >= 0) dec_tile_done<NT8>(a, cur_tile, facc, sub, par, lane, pend);
             cur_tile = tile;
 #pragma unroll
             for (int j = 0; j < NT8; ++j)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) facc[j][k] = 0.f;
         }
-        if ((i & 1) == par) {
-            const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
-            ptx::mbar_wait_u32(bar_full + 8 * s, ph);
-            if (sub < nsub && a.debug_skip == 0) {
-                const uint32_t st = stage0 + s * stage_bytes;
-#pragma unroll 2
-                for (int gi = 0; gi < n; ++gi)
-                    dec_group<WBITS, NT8, SPG, MODE, PARTIALS>(a, st, gi, g0 + gi, tile, nsub, facc, is16_mask);
-            }
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_u32(bar_empty + 8 * s);
+        const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
+        ptx::mbar_wait_u32(bar_full + 8 * s, ph);
+        if (a.trace && u == u0 && threadIdx.x == 0) trace_ev(a.trace, a.serial, 1, 3);
+        if (sub < nsub) {
+            const uint32_t st = stage0 + s * stage_bytes;
+#pragma unroll DEC_UNROLL
+            for (int gi = GSTEP == 1 ? 0 : par; gi < n; gi += GSTEP)
+                dec_group<WBITS, NT8, SPG, MODE, PARTIALS>(a, st, gi, g0 + gi, tile, nsub, facc, is16_mask);
         }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_u32(bar_empty + 8 * s);
+        if (!PARTIALS) dec_publish(pend, lane);
         if (++s == S) { s = 0; ph ^= 1; }
         u += n;
         g0 += n;
     }
     if constexpr (!PARTIALS) {
-        if (cur_tile >= 0) {
-            combine_parities<NT8>(facc, scr, par, sub, lane);
-            dec_flush<NT8>(a, cur_tile, facc, par ? 8 : sub, gid, t, s_flag);
-        }
+        if (cur_tile >= 0) dec_tile_done<NT8>(a, cur_tile, facc, sub, par, lane, pend);
+        dec_publish(pend, lane);
     }
+    if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 1, 4);
 }
 
 template <int WBITS, int NT8, int SPG, bool PARTIALS>
-__global__ void __launch_bounds__(DEC_THREADS) qlinear_decode_kernel(const DecArgs a) {
+__global__ void __launch_bounds__(DEC_THREADS, NT8 == 1 ? DEC_MINB : 1) qlinear_decode_kernel(const DecArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const WLayout& L = a.L;
     const int S = a.stages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
-    int* s_flag = reinterpret_cast<int*>(empty + S);
-    uint8_t* stage0 = smem + 128 * ((16 * S + 4 + 127) / 128);
+    uint8_t* stage0 = smem + 256;
     const int NG = L.NG;
     constexpr int G = SPG * 64;
+    constexpr int CPS = NT8 * 8 * G + NT8 * 64;
+    constexpr int X16S = NT8 * 8 * G * 2;
     const int U = L.T128 * NG;
     const int u0 = blockIdx.x * a.upc;
     const int u1 = min(U, u0 + a.upc);
@@ -449,9 +515,10 @@ __global__ void __launch_bounds__(DEC_THREADS) qlinear_decode_kernel(const DecAr
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], DEC_CWARPS / 2);  // the 8 warps of the stage's parity
+            ptx::mbar_init(&empty[s], DEC_CWARPS);
         }
         ptx::fence_mbar_init();
+        trace_ev(a.trace, a.serial, 1, 0);
     }
     __syncthreads();
     if (u0 >= u1) {
@@ -482,23 +549,14 @@ __global__ void __launch_bounds__(DEC_THREADS) qlinear_decode_kernel(const DecAr
             const int npre = i;
             // (2) activations: produced by the preceding kernels
             ptx::pdl_wait();
+            trace_ev(a.trace, a.serial, 1, 1);
             bool any16 = false;
             for (int m = 0; m < a.M; ++m) any16 |= ((a.row_bits ? a.row_bits[a.m0 + m] : a.bits) == 16);
             auto issue_a = [&](int s, int g0, int n) {
                 uint8_t* st = stage0 + (size_t)s * stage_bytes;
-                const uint32_t xb = (uint32_t)(n * 8 * G);
-                ptx::mbar_arrive_expect_tx(&full[s], n * 128 + NT8 * xb + (any16 ? NT8 * xb * 2 : 0));
-                ptx::bulk_g2s(st + a.off_par, a.ws + a.A.par_off + (size_t)g0 * 128, n * 128, &full[s]);
-#pragma unroll
-                for (int h = 0; h < NT8; ++h)
-                    ptx::bulk_g2s(st + a.off_xq + h * a.gps * 8 * G,
-                                  a.ws + a.A.xq_off + ((size_t)h * NG + g0) * 8 * G, xb, &full[s]);
-                if (any16) {
-#pragma unroll
-                    for (int h = 0; h < NT8; ++h)
-                        ptx::bulk_g2s(st + a.off_x16 + h * a.gps * 8 * G * 2,
-                                      a.ws + a.A.x16_off + ((size_t)h * NG + g0) * 8 * G * 2, xb * 2, &full[s]);
-                }
+                ptx::mbar_arrive_expect_tx(&full[s], n * CPS + (any16 ? n * X16S : 0));
+                ptx::bulk_g2s(st + a.off_cp, a.ws + a.A.cp_off + (size_t)g0 * CPS, n * CPS, &full[s]);
+                if (any16) ptx::bulk_g2s(st + a.off_x16, a.ws + a.A.x16_off + (size_t)g0 * X16S, n * X16S, &full[s]);
             };
             u = u0;
             for (int k = 0; k < npre; ++k) {
@@ -521,6 +579,7 @@ __global__ void __launch_bounds__(DEC_THREADS) qlinear_decode_kernel(const DecAr
             }
             // every weight byte of this CTA is in flight: let the next kernel's
             // CTAs launch (PDL trigger, one per CTA) so its producer can start
+            trace_ev(a.trace, a.serial, 1, 2);
             ptx::pdl_launch_dependents();
         }
         return;
@@ -552,21 +611,20 @@ __global__ void __launch_bounds__(DEC_THREADS) qlinear_decode_kernel(const DecAr
     any_int = __any_sync(0xffffffffu, any_int);
     const uint32_t bar_full = ptx::smem_u32(full), bar_empty = ptx::smem_u32(empty);
     const uint32_t st0 = ptx::smem_u32(stage0);
-    float* scr = reinterpret_cast<float*>(stage0 + (size_t)S * stage_bytes);
     if (!any16 && dec_call_centred(a.M, a.m0, a.row_bits, a.bits))
-        dec_consume<WBITS, NT8, SPG, MODE_INTC, PARTIALS>(a, bar_full, bar_empty, st0, s_flag, scr, u0, u1, is16_mask);
+        dec_consume<WBITS, NT8, SPG, MODE_INTC, PARTIALS>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
     else if (PARTIALS || (any_int && any16))
-        dec_consume<WBITS, NT8, SPG, MODE_MIXED, PARTIALS>(a, bar_full, bar_empty, st0, s_flag, scr, u0, u1, is16_mask);
+        dec_consume<WBITS, NT8, SPG, MODE_MIXED, PARTIALS>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
     else if (any16)
-        dec_consume<WBITS, NT8, SPG, MODE_A16, PARTIALS>(a, bar_full, bar_empty, st0, s_flag, scr, u0, u1, is16_mask);
+        dec_consume<WBITS, NT8, SPG, MODE_A16, PARTIALS>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
     else
-        dec_consume<WBITS, NT8, SPG, MODE_INT, PARTIALS>(a, bar_full, bar_empty, st0, s_flag, scr, u0, u1, is16_mask);
+        dec_consume<WBITS, NT8, SPG, MODE_INT, PARTIALS>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
 }
 
 // ------------------------------------------------------------------ host
 struct DecPlan {
     int upc, grid, gps, stages, stage_bytes;
-    int off_meta, off_par, off_xq, off_x16;
+    int off_meta, off_cp, off_x16;
     size_t smem;
 };
 
@@ -588,7 +646,9 @@ static int env_int(const char* name, int dflt) {
     return v ? atoi(v) : dflt;
 }
 
-// NT8 = 2 when M > 8 (two halves of 8 tokens)
+// Stage = gps units of one tile: codes | metadata | activation records | bf16 rows.
+// Shared memory budget 200 KB (one CTA per SM with 16 consumer warps); the
+// 8-warp build (-DDYQ_DEC_CWARPS=8) keeps <= 113 KB so two CTAs fit per SM.
 static DecPlan dec_plan(const WLayout& L, int nt8) {
     DecPlan p;
     const int unit_codes = (L.G / 64) * 8 * L.chunk;  // full tile
@@ -596,16 +656,16 @@ static DecPlan dec_plan(const WLayout& L, int nt8) {
     p.gps = (stage_code_kb * 1024) / unit_codes;
     if (p.gps < 1) p.gps = 1;
     if (p.gps > L.NG) p.gps = L.NG;
+    const int cps = nt8 * 8 * L.G + nt8 * 64, x16s = nt8 * 8 * L.G * 2;
     p.off_meta = p.gps * unit_codes;
-    p.off_par = p.off_meta + p.gps * META_BLOCK;
-    p.off_xq = p.off_par + p.gps * 128;
-    p.off_x16 = p.off_xq + nt8 * p.gps * 8 * L.G;
-    p.stage_bytes = p.off_x16 + nt8 * p.gps * 8 * L.G * 2;
-    static const int smem_kb = env_int("DYQ_DEC_SMEM_KB", 200);
-    p.stages = (smem_kb * 1024 - 256) / p.stage_bytes;
-    p.stages = p.stages < 2 ? 2 : (p.stages > 32 ? 32 : p.stages);
-    p.smem = 128 * ((16 * p.stages + 4 + 127) / 128) + (size_t)p.stages * p.stage_bytes +
-             (size_t)8 * 32 * 8 * 4;  // + parity-combine scratch
+    p.off_cp = p.off_meta + p.gps * META_BLOCK;
+    p.off_x16 = p.off_cp + p.gps * cps;
+    p.stage_bytes = p.off_x16 + p.gps * x16s;
+    static const int smem_kb1 = env_int("DYQ_DEC_SMEM_KB", 113);
+    const int smem_kb = (nt8 == 1 && DEC_CWARPS == 8) ? smem_kb1 : 200;
+    p.stages = (smem_kb * 1024 - 256 - 16 * 1024) / p.stage_bytes;
+    p.stages = p.stages < 2 ? 2 : (p.stages > 8 ? 8 : p.stages);
+    p.smem = 256 + (size_t)p.stages * p.stage_bytes + 8 * 32 * 8 * 4 + 8 * 1024;  // + combine + slot scratch
     const int U = L.T128 * L.NG;
     static const int ctas = env_int("DYQ_DEC_CTAS", 1);
     const int target = num_sms() * ctas;
@@ -615,10 +675,10 @@ static DecPlan dec_plan(const WLayout& L, int nt8) {
     return p;
 }
 
-// split-K slot storage: (grid + T128) slots of 16 x 128 floats, then T128 counters
+// split-K slot storage: (grid + T128) slots of 16 x 128 floats, then T128 x 8 counters
 size_t decode_ws_bytes(const WLayout& L) {
     const DecPlan p = dec_plan(L, 2);
-    return (size_t)(p.grid + L.T128) * 16 * 128 * 4 + (((size_t)L.T128 * 4 + 255) & ~(size_t)255);
+    return (size_t)(p.grid + L.T128) * 16 * 128 * 4 + (((size_t)L.T128 * 8 * 4 + 255) & ~(size_t)255);
 }
 
 template <int WBITS, int NT8, int SPG, bool PARTIALS>
@@ -647,13 +707,50 @@ static cudaError_t launch_k(const DecArgs& a, const DecPlan& p, cudaStream_t st)
     return a.L.G == 64 ? launch_k2<WBITS, NT8, 1, PARTIALS>(a, p, st) : launch_k2<WBITS, NT8, 2, PARTIALS>(a, p, st);
 }
 
+// L2 prefetch of a byte range (the next layer's packed weights): one thread per
+// CTA issues cp.async.bulk.prefetch.L2 over its slice and the CTA exits; the
+// HBM -> L2 transfer proceeds asynchronously while the dependent chain
+// (act-quant -> decode) of the current layer runs.  Reads nothing produced by
+// earlier kernels, so it triggers its dependents at once and never waits.
+__global__ void prefetch_l2_kernel(const uint8_t* p, size_t bytes, size_t per_cta) {
+    ptx::pdl_launch_dependents();
+    if (threadIdx.x != 0) return;
+    const size_t b0 = (size_t)blockIdx.x * per_cta;
+    const size_t b1 = b0 + per_cta < bytes ? b0 + per_cta : bytes;
+    for (size_t o = b0; o < b1; o += 32768) {
+        const uint32_t n = (uint32_t)((b1 - o) < 32768 ? (b1 - o) : 32768);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + o), "r"(n & ~15u) : "memory");
+    }
+}
+
+dyq_status_t launch_prefetch_l2(const void* p, size_t bytes, cudaStream_t st) {
+    if (bytes < 16) return DYQ_OK;
+    const int ctas = num_sms();
+    size_t per = (bytes + ctas - 1) / ctas;
+    per = (per + 4095) & ~(size_t)4095;
+    const unsigned grid = (unsigned)((bytes + per - 1) / per);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e =
+        cudaLaunchKernelEx(&cfg, prefetch_l2_kernel, reinterpret_cast<const uint8_t*>(p), bytes, per);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "prefetch_l2_kernel launch: %s", cudaGetErrorString(e));
+    return DYQ_OK;
+}
+
 // ws layout: [split-K slots + tile counters (decode_ws_bytes, zeroed once,
 // self-cleaning)] [activation area written by the quantizer kernel].
 dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int M,
                            int m0, const int32_t* row_bits, int bits, void* y, int y_dtype, int32_t* I_out,
                            void* ws, int64_t* /*err*/, cudaStream_t st) {
-    const int nt8 = M <= 8 ? 1 : 2;
-    const ActLayoutDec A = act_layout_dec(L);
+    const int nt8 = dec_nt8(M);
+    const ActLayoutDec A = act_layout_dec(L, nt8);
     const DecPlan p = dec_plan(L, nt8);
     const DecPlan p2 = dec_plan(L, 2);  // workspace is sized with the NT8 = 2 plan (same grid)
     DecArgs a;
@@ -678,11 +775,10 @@ dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta
     a.stages = p.stages;
     a.stage_bytes = p.stage_bytes;
     a.off_meta = p.off_meta;
-    a.off_par = p.off_par;
-    a.off_xq = p.off_xq;
+    a.off_cp = p.off_cp;
     a.off_x16 = p.off_x16;
-    static const int dbg = env_int("DYQ_DEBUG_SKIP", 0);
-    a.debug_skip = dbg;
+    a.trace = g_trace;
+    a.serial = g_trace_serial++;
     const bool partials = I_out != nullptr;
     cudaError_t e;
 #define DYQ_DISPATCH(WB)                                                                      \

@@ -12,7 +12,9 @@
 namespace dyq {
 
 static thread_local char g_err[512] = "";
-int g_path = 0;  // 0 auto, 1 decode, 2 prefill (read by the router)
+int g_path = 0;
+uint64_t* g_trace = nullptr;
+uint32_t g_trace_serial = 0;  // 0 auto, 1 decode, 2 prefill (read by the router)
 
 dyq_status_t set_error(dyq_status_t st, const char* fmt, ...) {
     va_list ap;
@@ -51,16 +53,6 @@ bool make_layout(const dyq_wdesc_t* wd, WLayout* L) {
     return true;
 }
 
-ActLayoutDec act_layout_dec(const WLayout& L) {
-    ActLayoutDec A;
-    A.par_off = 0;
-    A.xq_off = ((size_t)L.NG * DEC_MPAD * 8 + 255) & ~(size_t)255;
-    A.x16_off = A.xq_off + (((size_t)DEC_MPAD * L.K + 255) & ~(size_t)255);
-    A.zx_off = A.x16_off + (((size_t)DEC_MPAD * L.K * 2 + 255) & ~(size_t)255);
-    A.bytes = A.zx_off + (((size_t)L.NG * DEC_MPAD + 255) & ~(size_t)255);
-    return A;
-}
-
 static dyq_status_t validate_wdesc(const dyq_wdesc_t* wd, WLayout* L) {
     if (!wd) return set_error(DYQ_EINVAL, "null weight descriptor");
     if (wd->wbits != 4 && wd->wbits != 8)
@@ -85,6 +77,20 @@ extern "C" {
 
 const char* dyq_last_error(void) { return g_err; }
 const char* dyq_version(void) { return "dyq 0.1 sm_100a"; }
+
+// Debug trace of kernel timestamps (caller-owned device buffer; null disables).
+dyq_status_t dyq_trace_enable(void* dev_buf, int64_t bytes, dyq_stream_t stream) {
+    if (!dev_buf) {
+        g_trace = nullptr;
+        return DYQ_OK;
+    }
+    if (bytes < 64) return set_error(DYQ_EINVAL, "trace buffer too small");
+    const uint64_t hdr[2] = {0ull, (uint64_t)((bytes - 16) / 16)};
+    if (cudaMemcpyAsync(dev_buf, hdr, sizeof(hdr), cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
+        return check_launch("dyq_trace_enable");
+    g_trace = reinterpret_cast<uint64_t*>(dev_buf);
+    return DYQ_OK;
+}
 
 dyq_status_t dyq_set_path(int32_t path) {
     if (path < 0 || path > 2) return set_error(DYQ_EINVAL, "path must be 0, 1 or 2");
@@ -202,7 +208,7 @@ dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t tpe, const i
 // self-cleaning)] [standalone activation-quantizer output (dyq_act_quant)].
 static size_t act_area_offset(const WLayout& L) { return (decode_ws_bytes(L) + 255) & ~(size_t)255; }
 static size_t prefill_area_offset(const WLayout& L) {
-    return (act_area_offset(L) + act_layout_dec(L).bytes + 1023) & ~(size_t)1023;
+    return (act_area_offset(L) + act_layout_dec(L, 2).bytes + 1023) & ~(size_t)1023;
 }
 
 dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* bytes) {
@@ -284,6 +290,14 @@ dyq_status_t dyq_qlinear_i32_partials(const dyq_wdesc_t* wd, const void* codes, 
                                   ws_bytes);
     if (rc || M == 0) return rc;
     return run_decode(L, codes, meta, x, M, row_bits, bits, nullptr, 0, I, workspace, err, (cudaStream_t)stream);
+}
+
+// Asynchronous HBM -> L2 prefetch of packed weights (e.g. the next layer's
+// codes and metadata while the current layer's dependent chain runs).
+dyq_status_t dyq_prefetch_l2(const void* p, size_t bytes, dyq_stream_t stream) {
+    if (!p && bytes) return set_error(DYQ_EINVAL, "null pointer");
+    if (((uintptr_t)p & 15) != 0) return set_error(DYQ_EINVAL, "prefetch address must be 16-byte aligned");
+    return launch_prefetch_l2(p, bytes, (cudaStream_t)stream);
 }
 
 // Standalone quantizer into the workspace's activation area (inspection / reuse).

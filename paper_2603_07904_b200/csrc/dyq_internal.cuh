@@ -52,30 +52,44 @@ __host__ __device__ inline size_t meta_block(const WLayout& L, int tile, int g) 
 }
 __host__ __device__ inline int meta_slot(int sub, int r) { return sub * 16 + 2 * (r & 7) + (r >> 3); }
 
-// Activations for the decode kernel (<= 16 tokens, two halves of 8), laid out
-// so that a run of consecutive K-groups is contiguous in every array (one bulk
-// copy per array per pipeline stage):
-//   par [NG][16 tok] {float s_x; uint32 (z_x << 16) | SX}
-//   xq  [2 halves][NG][8 tok][G] u8 codes
-//   x16 [2 halves][NG][8 tok][G] bf16 copy of x for A16 (BF16-bypass) rows, else 0
+// Activations for the decode kernel (M <= 16 tokens per call, nt8 = M <= 8 ? 1 : 2
+// halves of 8 tokens).  Per K-group g one contiguous record of cp_stride bytes
+//   codes [nt8 halves][8 tok][G] u8 Eq. (2) codes (or centred s8, see below)
+//   par   [8 * nt8 tok] {float s_x; uint32 (z_x << 16) | SX  or  SXc}
+// so a run of consecutive K-groups is ONE bulk copy per pipeline stage; then
+//   x16 [NG][nt8 * 8 tok][G] bf16 copy of x for A16 (BF16-bypass) rows, else 0
+//   zx  [NG][16] u8 z_x (test hook only).
 // Inside each 64-k block the k order is permuted so that decode lane t reads
 // all of its B-fragment words with 16-byte loads:
 //   position t*16 + s*8 + h*4 + b  <->  k = 32*s + 16*h + 4*t + b
 // (u8 codes: one 16-B load; bf16: two 16-B loads), and the lane owning C-tokens
 // (2t, 2t+1) reads both tokens' parameters with one 16-B load.
 constexpr int DEC_MPAD = 16;
+__host__ __device__ inline int dec_nt8(int M) { return M <= 8 ? 1 : 2; }
 __host__ __device__ inline int dec_perm(int kk) {  // kk in [0,64) -> position
     const int s = kk >> 5, h = (kk >> 4) & 1, t = (kk >> 2) & 3, b = kk & 3;
     return t * 16 + s * 8 + h * 4 + b;
 }
 
 struct ActLayoutDec {
-    size_t par_off, xq_off, x16_off, zx_off, bytes;
+    size_t cp_off, x16_off, zx_off, bytes;
+    int nt8, cp_stride, x16_stride;
 };
+__host__ __device__ inline ActLayoutDec act_layout_dec(const WLayout& L, int nt8) {
+    ActLayoutDec A;
+    A.nt8 = nt8;
+    A.cp_stride = nt8 * 8 * L.G + nt8 * 8 * 8;
+    A.x16_stride = nt8 * 8 * L.G * 2;
+    A.cp_off = 0;
+    A.x16_off = ((size_t)L.NG * A.cp_stride + 255) & ~(size_t)255;
+    A.zx_off = A.x16_off + (((size_t)L.NG * A.x16_stride + 255) & ~(size_t)255);
+    A.bytes = A.zx_off + (((size_t)L.NG * DEC_MPAD + 255) & ~(size_t)255);
+    return A;
+}
 // Decode activation format of a call: CENTRED when every token of the call runs
 // at 2 or 4 bits -- codes stored as s8 (Xq - z_x) and par = {s_x, SXc = Sum (Xq - z_x)},
 // so the kernel needs one u8 x s8 IMMA and I = P' - z_w * SXc; otherwise RAW u8
-// codes with par = {s_x, z_x << 16 | SX}.  z_x is also kept in zx[NG][16] (test hook).
+// codes with par = {s_x, z_x << 16 | SX}.
 __device__ __forceinline__ bool dec_call_centred(int M, int m0, const int32_t* row_bits, int bits) {
     bool c = true;
     for (int m = 0; m < M; ++m) {
@@ -83,10 +97,6 @@ __device__ __forceinline__ bool dec_call_centred(int M, int m0, const int32_t* r
         c &= (b == 2 || b == 4);
     }
     return c;
-}
-// element offsets of token m, group g, in-group position pos
-__host__ __device__ inline size_t act_xq_index(int NG, int G, int m, int g, int pos) {
-    return (((size_t)(m >> 3) * NG + g) * 8 + (m & 7)) * G + pos;
 }
 
 // Prefill activation operand (M > 16): per (144-token tile, K-group) the UMMA
@@ -99,6 +109,23 @@ struct PreActLayout {
     size_t codes_off, x16_off, par_off, bytes;
     size_t codes_group, x16_group;
 };
+
+// ---------------------------------------------------------------- tracing
+// Optional %globaltimer event trace (dyq_trace_enable; debugging / profiling
+// only): buffer = [count][capacity][records of 2 x u64 {tag, ns}],
+// tag = serial << 32 | kernel << 24 | event << 16 | blockIdx.x.
+extern uint64_t* g_trace;   // host-side copy of the enabled buffer (or null)
+extern uint32_t g_trace_serial;
+__device__ __forceinline__ void trace_ev(uint64_t* tr, uint32_t serial, uint32_t kernel, uint32_t ev) {
+    if (!tr) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(tr), 1ull);
+    if (i < tr[1]) {
+        tr[2 + 2 * i] = ((uint64_t)serial << 32) | (kernel << 24) | (ev << 16) | (blockIdx.x & 0xffffu);
+        tr[3 + 2 * i] = t;
+    }
+}
 
 // ------------------------------------------------------------ error words
 __device__ inline void report_nonfinite(int64_t* err, int64_t idx) {
@@ -177,6 +204,7 @@ __device__ inline int warp_sum_i(int v) {
 }
 
 size_t decode_ws_bytes(const WLayout& L);
+dyq_status_t launch_prefetch_l2(const void* p, size_t bytes, cudaStream_t st);
 PreActLayout pre_act_layout(const WLayout& L, int M);
 dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, const int32_t* row_bits, int bits,
                                  void* act, int64_t* err, cudaStream_t st);
@@ -199,7 +227,6 @@ bool pdl_enabled();  // DYQ_NO_PDL=1 disables programmatic dependent launch (A/B
 dyq_status_t set_error(dyq_status_t st, const char* fmt, ...);
 dyq_status_t check_launch(const char* what);
 bool make_layout(const dyq_wdesc_t* wd, WLayout* L);
-ActLayoutDec act_layout_dec(const WLayout& L);
 
 // kernel launchers (one per TU)
 dyq_status_t launch_pack(const WLayout& L, const uint16_t* w, void* codes, void* meta,

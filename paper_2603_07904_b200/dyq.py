@@ -13,7 +13,7 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdyq.so")
+LIB_PATH = os.environ.get("DYQ_LIB") or os.path.join(_HERE, "libdyq.so")  # DYQ_LIB: A/B builds (tools/)
 
 P, i32, i64, f64, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_size_t
 
@@ -37,6 +37,8 @@ _SIGS = {
     "dyq_qlinear_i32_partials": [P, P, P, P, i32, P, i32, P, P, sz, P, P],
     "dyq_act_quant_for_check": [P, P, i32, P, i32, P, P, P, P, P, sz, P, P],
     "dyq_set_path": [i32],
+    "dyq_trace_enable": [P, i64, P],
+    "dyq_prefetch_l2": [P, sz, P],
     "dyq_act_quant": [P, P, i32, P, i32, P, sz, P, P],
     "dyq_qlinear_q": [P, P, P, P, i32, P, i32, P, i32, P, sz, P],
     "dyq_model_size": [P, P, P],
@@ -132,6 +134,28 @@ def version() -> str:
 
 def set_path(path: int):
     _call("dyq_set_path", path)
+
+
+def prefetch_l2(t, stream=None):
+    """dyq_prefetch_l2 over a whole device tensor."""
+    _call("dyq_prefetch_l2", _ptr(t), t.numel() * t.element_size(), _stream(stream))
+
+
+def trace_enable(buf, stream=None):
+    """Debug: record kernel %globaltimer events into a device uint8/int64 tensor
+    (None disables).  Read back with trace_read(buf)."""
+    _call("dyq_trace_enable", _ptr(buf), 0 if buf is None else buf.numel() * buf.element_size(), _stream(stream))
+
+
+def trace_read(buf):
+    """-> list of (serial, kernel, event, block, ns) from a trace buffer."""
+    import numpy as np
+    a = buf.view(__import__("torch").int64).cpu().numpy().view(np.uint64)
+    n = int(min(a[0], a[1]))
+    rec = a[2:2 + 2 * n].reshape(n, 2)
+    tag, t = rec[:, 0], rec[:, 1]
+    return [(int(g >> 32), int((g >> 24) & 0xff), int((g >> 16) & 0xff), int(g & 0xffff), int(ts))
+            for g, ts in zip(tag, t)]
 
 
 # ----------------------------------------------------------------- errors
@@ -254,6 +278,11 @@ class PackedLinear:
         meta = torch.empty(mb, dtype=torch.uint8, device=dev)
         pack_weights(wd, w_bf16, codes, meta, err, stream)
         return cls(wd, codes, meta)
+
+    def prefetch_l2(self, stream=None):
+        """Asynchronous HBM -> L2 prefetch of this layer's codes + metadata."""
+        prefetch_l2(self.codes, stream)
+        prefetch_l2(self.meta, stream)
 
     def workspace(self, M: int):
         import torch
