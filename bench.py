@@ -5,8 +5,8 @@ Workload (BASELINE.json configs[1], the config the metric's "qlinear HBM GB/s"
 is quoted on): one Llama-2-7B-shaped block (d=4096, ffn=11008) at decode,
 M action tokens (default 8), W4 (the paper's INT4-pinned weights).
 One STEP = one pass of the whole hot path for one control step:
-    dyq_select_bits (kinematic proxies -> S_t -> Alg. 1) on a[t-1]
-    -> dyq_route_bits (b* -> per-token activation bits, W4-pinned table)
+    dyq_select_route (kinematic proxies -> S_t -> Alg. 1 on a[t-1], then
+    b* -> per-token activation bits through the W4-pinned table, one kernel)
     -> for QKV, o, gate|up, down: dyq_act_quant + dyq_qlinear_q
 with b* chosen each step by the kinematic dispatcher from a synthetic
 LIBERO-shaped trajectory (120 untimed history steps first).
@@ -289,13 +289,12 @@ def main():
 
     bytes_step = sum(algo_bytes(N, K, M, G, WB) for _, N, K in lins)
     gate_li = [n for n, _, _ in lins].index("gate_up")
-    n_launch_step = 2 + 2 * len(lins)  # select_bits, route_bits, then act-quant + qlinear kernel per linear
+    n_launch_step = 1 + 2 * len(lins)  # select_route, then act-quant + qlinear kernel per linear
 
     def step(t, fixed_bits=None, ev=None):
         c = t % C
         if fixed_bits is None:
-            dyq.select_bits(state, 1, acts[t - 1], bits)
-            dyq.route_bits(bits, 1, M, row_bits)
+            dyq.select_route(state, 1, acts[t - 1], bits, M, row_bits)
             rb, b = row_bits, 0
         else:
             rb, b = None, fixed_bits
@@ -548,8 +547,7 @@ def main():
             a_dev.copy_(a_host[t - 1], non_blocking=True)
             for li in range(len(lins)):
                 x_dev[li].copy_(x_host[t % 8][li], non_blocking=True)
-            dyq.select_bits(state, 1, a_dev, bits)
-            dyq.route_bits(bits, 1, M, row_bits)
+            dyq.select_route(state, 1, a_dev, bits, M, row_bits)
             for li, (name, N, K) in enumerate(lins):
                 p = packed[t % C][li]
                 dyq.qlinear(p.wd, p.codes, p.meta, x_dev[li], M, row_bits, 0, ys[li], 1, wss[li])

@@ -150,6 +150,13 @@ DYQ_API dyq_status_t dyq_state_reset_episode(void* state, const uint8_t* mask,
 DYQ_API dyq_status_t dyq_select_bits(void* state, int32_t E, const float* prev_action,
                              int32_t* bits, double* S_out, int32_t* target_out,
                              dyq_stream_t stream);
+/* dyq_select_bits fused with dyq_route_bits (one kernel per control step):
+ * also writes row_bits[e * tokens_per_episode + i] = abits_of(bits[e]) for
+ * i < tokens_per_episode.  Same state / outputs / errors as the two calls. */
+DYQ_API dyq_status_t dyq_select_route(void* state, int32_t E, const float* prev_action,
+                              int32_t* bits, int32_t tokens_per_episode,
+                              const int32_t* abits_of_host /* [4] or NULL */, int32_t* row_bits,
+                              double* S_out, int32_t* target_out, dyq_stream_t stream);
 /* Expand per-episode bits to per-token activation bits through the variant
  * table (DESIGN.md conflict C1): row_bits[m] = abits_of(bits[m / tokens_per_episode]).
  * abits_of maps b* in {2,4,8,16} -> activation bits; pass NULL for identity

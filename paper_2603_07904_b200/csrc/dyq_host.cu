@@ -189,7 +189,24 @@ dyq_status_t dyq_select_bits(void* state, int32_t E, const float* prev_action, i
                              int32_t* target_out, dyq_stream_t stream) {
     if (!state || !bits) return set_error(DYQ_EINVAL, "null pointer");
     if (E <= 0 || E > (1 << 20)) return set_error(DYQ_ESHAPE, "E out of range");
-    return launch_select(state, E, 1024, prev_action, bits, S_out, target_out, (cudaStream_t)stream);
+    return launch_select(state, E, nullptr, prev_action, bits, S_out, target_out, 0, nullptr, nullptr,
+                         (cudaStream_t)stream);
+}
+
+dyq_status_t dyq_select_route(void* state, int32_t E, const float* prev_action, int32_t* bits,
+                              int32_t tokens_per_episode, const int32_t* abits_of_host, int32_t* row_bits,
+                              double* S_out, int32_t* target_out, dyq_stream_t stream) {
+    if (!state || !bits || !row_bits) return set_error(DYQ_EINVAL, "null pointer");
+    if (E <= 0 || E > (1 << 20)) return set_error(DYQ_ESHAPE, "E out of range");
+    if (tokens_per_episode <= 0) return set_error(DYQ_ESHAPE, "tokens_per_episode must be positive");
+    if (abits_of_host)
+        for (int i = 0; i < 4; ++i) {
+            const int b = abits_of_host[i];
+            if (b != 2 && b != 4 && b != 8 && b != 16)
+                return set_error(DYQ_EINVAL, "abits_of[%d] = %d not in {2,4,8,16}", i, b);
+        }
+    return launch_select(state, E, nullptr, prev_action, bits, S_out, target_out, tokens_per_episode, abits_of_host,
+                         row_bits, (cudaStream_t)stream);
 }
 
 dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t tpe, const int32_t* abits_of_host,

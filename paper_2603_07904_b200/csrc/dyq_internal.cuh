@@ -215,8 +215,9 @@ extern int g_path;
 size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
 dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);
 dyq_status_t launch_sel_reset(void* state, int32_t E, const uint8_t* mask, cudaStream_t st);
-dyq_status_t launch_select(void* state, int32_t E, int32_t H, const float* prev_action, int32_t* bits,
-                           double* S_out, int32_t* target_out, cudaStream_t st);
+dyq_status_t launch_select(void* state, int32_t E, const dyq_calib_t* cal_or_null, const float* prev_action,
+                           int32_t* bits, double* S_out, int32_t* target_out, int32_t tpe, const int32_t* tab4,
+                           int32_t* row_bits, cudaStream_t st);
 dyq_status_t launch_route(const int32_t* bits, int32_t E, int32_t tpe, const int32_t* tab4, int32_t* row_bits,
                           cudaStream_t st);
 }  // namespace dyq
@@ -253,8 +254,9 @@ extern int g_path;
 size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
 dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);
 dyq_status_t launch_sel_reset(void* state, int32_t E, const uint8_t* mask, cudaStream_t st);
-dyq_status_t launch_select(void* state, int32_t E, int32_t H, const float* prev_action, int32_t* bits,
-                           double* S_out, int32_t* target_out, cudaStream_t st);
+dyq_status_t launch_select(void* state, int32_t E, const dyq_calib_t* cal_or_null, const float* prev_action,
+                           int32_t* bits, double* S_out, int32_t* target_out, int32_t tpe, const int32_t* tab4,
+                           int32_t* row_bits, cudaStream_t st);
 dyq_status_t launch_route(const int32_t* bits, int32_t E, int32_t tpe, const int32_t* tab4, int32_t* row_bits,
                           cudaStream_t st);
 }  // namespace dyq

@@ -549,8 +549,7 @@ dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t
     for (int i = 0; i < 4; ++i) wd[i] = wdesc_of(D, i);
 
     // b*_t from a_{t-1}, then per-row activation bits (W4-pinned table)
-    DYQ_TRY(dyq_select_bits(state, E, m->t == 0 ? nullptr : prev, bits, nullptr, nullptr, stream));
-    DYQ_TRY(dyq_route_bits(bits, E, S, nullptr, rbp, stream));
+    DYQ_TRY(dyq_select_route(state, E, m->t == 0 ? nullptr : prev, bits, S, nullptr, rbp, nullptr, nullptr, stream));
     DYQ_TRY(dyq_route_bits(bits, E, 1, nullptr, rbd, stream));
 
     auto layer = [&](int l, int M, int32_t* rb, bool prefill, int pos) -> dyq_status_t {

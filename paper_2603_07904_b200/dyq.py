@@ -31,6 +31,7 @@ _SIGS = {
     "dyq_state_reset_episode": [P, P, P],
     "dyq_select_bits": [P, i32, P, P, P, P, P],
     "dyq_route_bits": [P, i32, i32, P, P, P],
+    "dyq_select_route": [P, i32, P, P, i32, P, P, P, P, P],
     "dyq_qlinear_workspace": [P, i32, P],
     "dyq_workspace_init": [P, sz, P],
     "dyq_qlinear": [P, P, P, P, i32, P, i32, P, i32, P, sz, P, P],
@@ -209,6 +210,14 @@ def state_reset_episode(state, mask=None, stream=None):
 def select_bits(state, E: int, prev_action, bits, S_out=None, target_out=None, stream=None):
     _call("dyq_select_bits", _ptr(state), E, _ptr(prev_action), _ptr(bits), _ptr(S_out),
           _ptr(target_out), _stream(stream))
+
+
+def select_route(state, E: int, prev_action, bits, tokens_per_episode: int, row_bits, abits_of=None,
+                 S_out=None, target_out=None, stream=None):
+    """dyq_select_bits + dyq_route_bits in one kernel."""
+    tab = (i32 * 4)(*abits_of) if abits_of is not None else None
+    _call("dyq_select_route", _ptr(state), E, _ptr(prev_action), _ptr(bits), tokens_per_episode, tab,
+          _ptr(row_bits), _ptr(S_out), _ptr(target_out), _stream(stream))
 
 
 def route_bits(bits, E: int, tokens_per_episode: int, row_bits, abits_of=None, stream=None):

@@ -269,6 +269,38 @@ def test_select_bits_bit_exact_calibs(kw):
     assert np.array_equal(bits, ref["bits"])
 
 
+@pytest.mark.parametrize("H", [7, 256])
+def test_select_bits_ties_in_history(H):
+    # actions on a coarse grid: many equal magnitudes / jerks in the p95 ring, so
+    # the sorted-ring update deletes and inserts duplicates (ring wraps 40x at H=7)
+    acts = np.round(synth.trajectories(3, 300, seed0=5000) * 4.0) / 4.0
+    acts[100:140] = 0.0  # a stretch of zero motion (mag = jerk = 0)
+    kw = dict(H=H, W_macro=5, W_micro=3)
+    ref = oracle.replay(acts, oracle.default_calib(**kw))
+    bits, tgt, S = _gpu_replay(acts, kw)
+    assert np.array_equal(S.view(np.uint64), ref["S"].view(np.uint64))
+    assert np.array_equal(bits, ref["bits"])
+
+
+def test_select_route_matches_select_then_route():
+    E, T, tpe = 6, 60, 5
+    acts = synth.trajectories(E, T, seed0=6000)
+    ref = oracle.replay(acts)
+    cal = dyq.default_calib()
+    st = torch.zeros(dyq.state_size(E, cal), dtype=torch.uint8, device=DEV)
+    dyq.state_init(E, cal, st)
+    a = torch.from_numpy(np.ascontiguousarray(acts, np.float32)).to(DEV)
+    bits = torch.zeros(E, dtype=torch.int32, device=DEV)
+    rb = torch.zeros(E * tpe, dtype=torch.int32, device=DEV)
+    tab = (4, 4, 8, 16)
+    for t in range(T):
+        dyq.select_route(st, E, None if t == 0 else a[t - 1], bits, tpe, rb, abits_of=tab)
+        b = bits.cpu().numpy()
+        assert np.array_equal(b, ref["bits"][t])
+        want = np.repeat([{2: 4, 4: 4, 8: 8, 16: 16}[int(v)] for v in b], tpe)
+        assert np.array_equal(rb.cpu().numpy(), want)
+
+
 def test_select_bits_episode_reset_keeps_history():
     acts = synth.trajectories(4, 80, seed0=4000)
     bits, tgt, S = _gpu_replay(acts, reset_at=40)
