@@ -1,6 +1,7 @@
 """Per-kernel share of the timed step from an ncu launch list (gpu__time_duration.sum),
-keeping only launches from the first route_bits_kernel on (the 120 untimed
-select_bits history steps come before it).  usage: launch_summary.py launches.csv > out.json"""
+keeping only complete steps: select_bits_kernel (fused select+route) followed by
+(act-quant, qlinear) x 4 (the 120 untimed select_bits history steps have no
+qlinear after them).  usage: launch_summary.py launches.csv > out.json"""
 import csv
 import json
 import sys
@@ -8,14 +9,14 @@ from collections import defaultdict
 
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10 and r[0] != "ID"]
 rows = [r for r in rows if r[-3] == "gpu__time_duration.sum"]
-# keep complete steps only: select_bits, route_bits, then (act-quant, qlinear) x 4
+# keep complete steps only: select_bits (+route), then (act-quant, qlinear) x 4
 names = [r[4] for r in rows]
 keep = []
 i = 0
-while i + 10 <= len(rows):
-    if "select_bits_kernel" in names[i] and "route_bits_kernel" in names[i + 1]:
-        keep.extend(rows[i:i + 10])
-        i += 10
+while i + 9 <= len(rows):
+    if "select_bits_kernel" in names[i] and "actquant_dec_kernel" in names[i + 1]:
+        keep.extend(rows[i:i + 9])
+        i += 9
     else:
         i += 1
 rows = keep
