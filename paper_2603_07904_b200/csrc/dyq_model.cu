@@ -57,6 +57,69 @@ __global__ void add_rmsnorm_kernel(uint16_t* __restrict__ h, const uint16_t* __r
     }
 }
 
+// Same op, one 16-B vector of 8 elements per thread (d = 8 * blockDim.x), h
+// kept in registers between the statistics and the output pass; PDL-launched.
+__global__ void __launch_bounds__(1024) add_rmsnorm8_kernel(uint16_t* __restrict__ h,
+                                                            const uint16_t* __restrict__ delta,
+                                                            const uint16_t* __restrict__ w, int d, float eps,
+                                                            uint16_t* __restrict__ y) {
+    __shared__ float red[32];
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    const size_t o = (size_t)blockIdx.x * d + threadIdx.x * 8;
+    const uint4 hv = *reinterpret_cast<const uint4*>(h + o);
+    const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+    float a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = bf2f((uint16_t)(hw[k >> 1] >> (16 * (k & 1))));
+    if (delta) {
+        const uint4 dv = *reinterpret_cast<const uint4*>(delta + o);
+        const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w};
+        uint32_t nh[4];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            const uint16_t lo = f2bf(a[k] + bf2f((uint16_t)(dw[k >> 1] & 0xffffu)));
+            const uint16_t hi = f2bf(a[k + 1] + bf2f((uint16_t)(dw[k >> 1] >> 16)));
+            a[k] = bf2f(lo);
+            a[k + 1] = bf2f(hi);
+            nh[k >> 1] = (uint32_t)lo | ((uint32_t)hi << 16);
+        }
+        *reinterpret_cast<uint4*>(h + o) = make_uint4(nh[0], nh[1], nh[2], nh[3]);
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) ss += a[k] * a[k] + a[k + 1] * a[k + 1];
+    const float inv = rsqrtf(block_sum(ss, red) / (float)d + eps);
+    const uint4 wv = *reinterpret_cast<const uint4*>(w + threadIdx.x * 8);
+    const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+    uint32_t yo[4];
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+        const uint16_t lo = f2bf(a[k] * inv * bf2f((uint16_t)(ww[k >> 1] & 0xffffu)));
+        const uint16_t hi = f2bf(a[k + 1] * inv * bf2f((uint16_t)(ww[k >> 1] >> 16)));
+        yo[k >> 1] = (uint32_t)lo | ((uint32_t)hi << 16);
+    }
+    *reinterpret_cast<uint4*>(y + o) = make_uint4(yo[0], yo[1], yo[2], yo[3]);
+}
+
+// Launch with programmatic dependent launch (every kernel launched this way
+// calls griddepcontrol.wait before reading anything a previous kernel wrote).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // rotate_half RoPE on the q and k parts: pairs (i, i + HD/2) of every head
 __global__ void rope_kernel(uint16_t* __restrict__ qkv, int M, int S, int pos0, int d, int H, float theta) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -162,6 +225,185 @@ __global__ void __launch_bounds__(256) attn_prefill_kernel(const uint16_t* __res
     }
 }
 
+// Causal prefill attention on the tensor cores (mma.sync m16n8k16 bf16 -> fp32,
+// FlashAttention-2 style online softmax).  CTA = (64-query block, head,
+// episode), 4 warps x 16 queries; Q fragments stay in registers, K / V blocks of
+// 64 keys are staged in shared memory (row stride 136 bf16: conflict-free
+// ldmatrix), S = Q K^T and O += P V with P re-packed from the S accumulators.
+// The CTA also writes its own 64 keys' K / V rows into the KV cache.
+constexpr int FQ = 64, FK = 64, FST = HD + 8;  // query / key block, smem row stride (bf16)
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+    return (uint32_t)f2bf(lo) | ((uint32_t)f2bf(hi) << 16);
+}
+__global__ void __launch_bounds__(128) attn_prefill_tc_kernel(const uint16_t* __restrict__ qkv, int S, int d, int H,
+                                                              uint16_t* __restrict__ kv, int layer, int L, int T,
+                                                              uint16_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint16_t fs[];
+    uint16_t* Qs = fs;              // [FQ][FST]
+    uint16_t* Ks = Qs + FQ * FST;   // [FK][FST]
+    uint16_t* Vs = Ks + FK * FST;   // [FK][FST]
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    const int q0 = blockIdx.x * FQ, hh = blockIdx.y, e = blockIdx.z;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const size_t rs = (size_t)3 * d;
+    const uint16_t* base = qkv + (size_t)e * S * rs + hh * HD;
+    // ---- Q tile -> smem -> fragments (8 k-steps of 16 dims)
+    for (int i = tid; i < FQ * (HD / 8); i += 128) {
+        const int r = i / (HD / 8), c = (i % (HD / 8)) * 8;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (q0 + r < S) v = *reinterpret_cast<const uint4*>(base + (size_t)(q0 + r) * rs + c);
+        *reinterpret_cast<uint4*>(Qs + r * FST + c) = v;
+    }
+    __syncthreads();
+    uint32_t qf[HD / 16][4];
+    {
+        const uint32_t qb = ptx::smem_u32(Qs + (warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * FST + (lane >> 4) * 8);
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) ldsm_x4(qb + ks * 32, qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3]);
+    }
+    float o[HD / 8][4];
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows g and g + 8 of this warp
+    const float sl2 = rsqrtf((float)HD) * 1.4426950408889634f;  // scale * log2(e)
+    const int qr0 = q0 + warp * 16 + g, qr1 = qr0 + 8;
+    const int kb_last = min(q0 + FQ - 1, S - 1) / FK;
+    for (int kb = 0; kb <= kb_last; ++kb) {
+        const int k0 = kb * FK;
+        __syncthreads();  // previous block's K / V reads done
+        for (int i = tid; i < FK * (HD / 8); i += 128) {
+            const int r = i / (HD / 8), c = (i % (HD / 8)) * 8;
+            uint4 kk = make_uint4(0u, 0u, 0u, 0u), vv = kk;
+            if (k0 + r < S) {
+                kk = *reinterpret_cast<const uint4*>(base + (size_t)(k0 + r) * rs + d + c);
+                vv = *reinterpret_cast<const uint4*>(base + (size_t)(k0 + r) * rs + 2 * d + c);
+                if (k0 + r >= q0 && k0 + r < q0 + FQ) {  // this CTA's keys go to the KV cache
+                    *reinterpret_cast<uint4*>(kv + kv_off(e, layer, 0, k0 + r, L, T, d) + hh * HD + c) = kk;
+                    *reinterpret_cast<uint4*>(kv + kv_off(e, layer, 1, k0 + r, L, T, d) + hh * HD + c) = vv;
+                }
+            }
+            *reinterpret_cast<uint4*>(Ks + r * FST + c) = kk;
+            *reinterpret_cast<uint4*>(Vs + r * FST + c) = vv;
+        }
+        __syncthreads();
+        // ---- S = Q K^T: 8 n-tiles of 8 keys
+        float sacc[FK / 8][4];
+#pragma unroll
+        for (int j = 0; j < FK / 8; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+        const uint32_t kbse = ptx::smem_u32(Ks + ((lane & 7) + (lane >> 4) * 8) * FST + ((lane >> 3) & 1) * 8);
+#pragma unroll
+        for (int jp = 0; jp < FK / 16; ++jp) {  // pairs of n-tiles
+#pragma unroll
+            for (int ks = 0; ks < HD / 16; ++ks) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(kbse + (jp * 16 * FST + ks * 16) * 2, b0, b1, b2, b3);
+                mma16816(sacc[2 * jp], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b0, b1);
+                mma16816(sacc[2 * jp + 1], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b2, b3);
+            }
+        }
+        // ---- causal mask, online softmax (base 2)
+        float bm0 = -INFINITY, bm1 = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < FK / 8; ++j) {
+            const int kc = k0 + j * 8 + 2 * t;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                sacc[j][u] = (kc + u <= qr0 && kc + u < S) ? sacc[j][u] * sl2 : -INFINITY;
+                sacc[j][2 + u] = (kc + u <= qr1 && kc + u < S) ? sacc[j][2 + u] * sl2 : -INFINITY;
+                bm0 = fmaxf(bm0, sacc[j][u]);
+                bm1 = fmaxf(bm1, sacc[j][2 + u]);
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < 4; off <<= 1) {
+            bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, off));
+            bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, off));
+        }
+        const float nm0 = fmaxf(m0, bm0), nm1 = fmaxf(m1, bm1);
+        // rows with no visible key yet keep m = -inf: use 0 as the exponent base there
+        const float b0e = nm0 == -INFINITY ? 0.f : nm0, b1e = nm1 == -INFINITY ? 0.f : nm1;
+        const float c0 = exp2f(m0 - b0e), c1 = exp2f(m1 - b1e);
+        m0 = nm0;
+        m1 = nm1;
+        float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < FK / 8; ++j) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                sacc[j][u] = exp2f(sacc[j][u] - b0e);
+                sacc[j][2 + u] = exp2f(sacc[j][2 + u] - b1e);
+                rs0 += sacc[j][u];
+                rs1 += sacc[j][2 + u];
+            }
+        }
+        l0 = l0 * c0 + rs0;
+        l1 = l1 * c1 + rs1;
+#pragma unroll
+        for (int i = 0; i < HD / 8; ++i) {
+            o[i][0] *= c0;
+            o[i][1] *= c0;
+            o[i][2] *= c1;
+            o[i][3] *= c1;
+        }
+        // ---- O += P V: 4 k-steps of 16 keys, 16 dim-tiles of 8
+        const uint32_t vbse = ptx::smem_u32(Vs + ((lane & 7) + ((lane >> 3) & 1) * 8) * FST + (lane >> 4) * 8);
+#pragma unroll
+        for (int kk = 0; kk < FK / 16; ++kk) {
+            // P = P_hi + P_lo, both bf16 (the fp32 probabilities to ~2^-16
+            // relative): two MMAs per V fragment instead of one bf16-rounded P
+            uint32_t ah[4], al[4];
+            const float* pv[4] = {&sacc[2 * kk][0], &sacc[2 * kk][2], &sacc[2 * kk + 1][0], &sacc[2 * kk + 1][2]};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint16_t h0 = f2bf(pv[r][0]), h1 = f2bf(pv[r][1]);
+                ah[r] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+                al[r] = pack_bf2(pv[r][0] - bf2f(h0), pv[r][1] - bf2f(h1));
+            }
+#pragma unroll
+            for (int np = 0; np < HD / 16; ++np) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(vbse + (kk * 16 * FST + np * 16) * 2, b0, b1, b2, b3);
+                mma16816(o[2 * np], ah[0], ah[1], ah[2], ah[3], b0, b1);
+                mma16816(o[2 * np + 1], ah[0], ah[1], ah[2], ah[3], b2, b3);
+                mma16816(o[2 * np], al[0], al[1], al[2], al[3], b0, b1);
+                mma16816(o[2 * np + 1], al[0], al[1], al[2], al[3], b2, b3);
+            }
+        }
+    }
+    // ---- normalise and store (rows qr0, qr1)
+#pragma unroll
+    for (int off = 1; off < 4; off <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    }
+    const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+        const int c = hh * HD + i * 8 + 2 * t;
+        if (qr0 < S)
+            *reinterpret_cast<uint32_t*>(out + ((size_t)e * S + qr0) * d + c) = pack_bf2(o[i][0] * i0, o[i][1] * i0);
+        if (qr1 < S)
+            *reinterpret_cast<uint32_t*>(out + ((size_t)e * S + qr1) * d + c) = pack_bf2(o[i][2] * i1, o[i][3] * i1);
+    }
+}
+
 // Decode attention: CTA = (head, episode); the new token's K, V are written to
 // the cache at `pos`, then softmax(q K^T) V over positions 0..pos.
 __global__ void __launch_bounds__(256) attn_decode_kernel(const uint16_t* __restrict__ qkv, int pos, int d, int H,
@@ -229,6 +471,112 @@ __global__ void __launch_bounds__(256) attn_decode_kernel(const uint16_t* __rest
         const float o = part[threadIdx.x] + part[HD + threadIdx.x] + part[2 * HD + threadIdx.x] +
                         part[3 * HD + threadIdx.x];
         out[(size_t)e * d + hh * HD + threadIdx.x] = f2bf(o / sum);
+    }
+}
+
+// Decode attention, latency-optimised: CTA = (head, episode), 512 threads.
+// Scores: one thread per key with the whole 256-B key row in flight (16
+// independent 16-B loads) before the dot product; P V: thread = (8-dim chunk,
+// key slice of 32), 16-B value loads, partial sums reduced through shared
+// memory.  PDL-launched.
+constexpr int ADT = 512;
+__global__ void __launch_bounds__(ADT) attn_decode2_kernel(const uint16_t* __restrict__ qkv, int pos, int d, int H,
+                                                           uint16_t* __restrict__ kv, int layer, int L, int T,
+                                                           uint16_t* __restrict__ out) {
+    extern __shared__ __align__(16) float smf[];
+    float* qsh = smf;            // [HD]
+    float* red = qsh + HD;       // [32]
+    float* part = red + 32;      // [32 slices][HD]
+    float* ps = part + 32 * HD;  // [pos + 1]
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    const int hh = blockIdx.x, e = blockIdx.y;
+    const size_t rs = (size_t)3 * d;
+    const uint16_t* row = qkv + (size_t)e * rs;
+    uint16_t* Kc = kv + kv_off(e, layer, 0, 0, L, T, d) + hh * HD;
+    uint16_t* Vc = kv + kv_off(e, layer, 1, 0, L, T, d) + hh * HD;
+    const float scale = rsqrtf((float)HD);
+    const int tid = threadIdx.x;
+    if (tid < HD / 8) {
+        *reinterpret_cast<uint4*>(Kc + (size_t)pos * d + tid * 8) =
+            *reinterpret_cast<const uint4*>(row + d + hh * HD + tid * 8);
+        *reinterpret_cast<uint4*>(Vc + (size_t)pos * d + tid * 8) =
+            *reinterpret_cast<const uint4*>(row + 2 * d + hh * HD + tid * 8);
+    }
+    if (tid < HD) qsh[tid] = bf2f(row[hh * HD + tid]) * scale;
+    __syncthreads();
+    float mx = -INFINITY;
+    for (int j = tid; j <= pos; j += ADT) {
+        const uint4* kr = reinterpret_cast<const uint4*>(Kc + (size_t)j * d);
+        float s = 0.f;
+#pragma unroll
+        for (int hlf = 0; hlf < 2; ++hlf) {  // 8 x 16-B loads in flight, then 64 FMAs
+            uint4 k8[HD / 16];
+#pragma unroll
+            for (int c = 0; c < HD / 16; ++c) k8[c] = kr[hlf * (HD / 16) + c];
+#pragma unroll
+            for (int c = 0; c < HD / 16; ++c) {
+                const uint32_t kk[4] = {k8[c].x, k8[c].y, k8[c].z, k8[c].w};
+                const int cb = (hlf * (HD / 16) + c) * 8;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    s = fmaf(qsh[cb + 2 * u], __uint_as_float(kk[u] << 16), s);
+                    s = fmaf(qsh[cb + 2 * u + 1], __uint_as_float(kk[u] & 0xffff0000u), s);
+                }
+            }
+        }
+        ps[j] = s;
+        mx = fmaxf(mx, s);
+    }
+    mx = warp_max(mx);
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int i = 1; i < ADT / 32; ++i) mx = fmaxf(mx, red[i]);
+    __syncthreads();
+    float sum = 0.f;
+    for (int j = tid; j <= pos; j += ADT) {
+        const float p = __expf(ps[j] - mx);
+        ps[j] = p;
+        sum += p;
+    }
+    sum = block_sum(sum, red);  // (contains the barrier that publishes ps)
+    const int c8 = tid & 15, sl = tid >> 4;  // 16 chunks of 8 dims x 32 key slices
+    float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int j = sl;
+    for (; j + 96 <= pos; j += 128) {  // 4 keys per iteration, loads first
+        uint4 v4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v4[u] = *reinterpret_cast<const uint4*>(Vc + (size_t)(j + 32 * u) * d + c8 * 8);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float p = ps[j + 32 * u];
+            const uint32_t vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                o[2 * k] = fmaf(p, __uint_as_float(vv[k] << 16), o[2 * k]);
+                o[2 * k + 1] = fmaf(p, __uint_as_float(vv[k] & 0xffff0000u), o[2 * k + 1]);
+            }
+        }
+    }
+    for (; j <= pos; j += 32) {
+        const uint4 v = *reinterpret_cast<const uint4*>(Vc + (size_t)j * d + c8 * 8);
+        const float p = ps[j];
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            o[2 * k] = fmaf(p, __uint_as_float(vv[k] << 16), o[2 * k]);
+            o[2 * k + 1] = fmaf(p, __uint_as_float(vv[k] & 0xffff0000u), o[2 * k + 1]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) part[sl * HD + c8 * 8 + k] = o[k];
+    __syncthreads();
+    if (tid < HD) {
+        float acc = 0.f;
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) acc += part[q * HD + tid];
+        out[(size_t)e * d + hh * HD + tid] = f2bf(acc / sum);
     }
 }
 
@@ -411,6 +759,13 @@ dyq_status_t dyq_add_rmsnorm(uint16_t* h, const uint16_t* delta, const uint16_t*
     if (M < 0 || d <= 0 || d % 2) return set_error(DYQ_ESHAPE, "bad rmsnorm shape");
     if (M == 0) return DYQ_OK;
     if (!h || !w || !y) return set_error(DYQ_EINVAL, "null pointer");
+    const bool al = ((uintptr_t)h | (uintptr_t)w | (uintptr_t)y | (uintptr_t)delta) % 16 == 0;
+    if (d % 256 == 0 && d / 8 <= 1024 && al) {
+        const cudaError_t e = launch_pdl(add_rmsnorm8_kernel, dim3(M), dim3(d / 8), 0, (cudaStream_t)stream, h, delta,
+                                         w, d, eps, y);
+        if (e != cudaSuccess) return set_error(DYQ_ECUDA, "add_rmsnorm8_kernel: %s", cudaGetErrorString(e));
+        return check_launch("add_rmsnorm8_kernel");
+    }
     add_rmsnorm_kernel<<<M, 256, 0, (cudaStream_t)stream>>>(h, delta, w, d, eps, y);
     return check_launch("add_rmsnorm_kernel");
 }
@@ -428,6 +783,18 @@ dyq_status_t dyq_attention_prefill(const uint16_t* qkv, int32_t E, int32_t S, in
                                    int32_t layer, int32_t L, int32_t T, uint16_t* out, dyq_stream_t stream) {
     if (E <= 0 || S <= 0 || S > T || d != H * HD || layer < 0 || layer >= L)
         return set_error(DYQ_ESHAPE, "bad attention shape");
+    if (d % 8 == 0 && ((uintptr_t)qkv | (uintptr_t)kv | (uintptr_t)out) % 16 == 0) {
+        const size_t smem_tc = (size_t)(FQ + 2 * FK) * FST * 2;
+        static bool attr_tc = false;
+        if (!attr_tc) {
+            cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc);
+            attr_tc = true;
+        }
+        const cudaError_t e = launch_pdl(attn_prefill_tc_kernel, dim3((S + FQ - 1) / FQ, H, E), dim3(128), smem_tc,
+                                         (cudaStream_t)stream, qkv, S, d, H, kv, layer, L, T, out);
+        if (e != cudaSuccess) return set_error(DYQ_ECUDA, "attn_prefill_tc_kernel: %s", cudaGetErrorString(e));
+        return check_launch("attn_prefill_tc_kernel");
+    }
     const size_t smem = attn_ks_bytes(S) + (size_t)S * HD * 2 + 8 * HD * 4 + (size_t)8 * S * 4;
     if (smem > 227 * 1024) return set_error(DYQ_EUNSUPPORTED, "attention prefill: S = %d too long", S);
     static bool attr = false;
@@ -444,6 +811,20 @@ dyq_status_t dyq_attention_decode(const uint16_t* qkv, int32_t E, int32_t pos, i
                                   int32_t layer, int32_t L, int32_t T, uint16_t* out, dyq_stream_t stream) {
     if (E <= 0 || pos < 0 || pos >= T || d != H * HD || layer < 0 || layer >= L)
         return set_error(DYQ_ESHAPE, "bad attention shape");
+    if (d % 8 == 0 && ((uintptr_t)qkv | (uintptr_t)kv) % 16 == 0) {
+        const size_t smem2 = (HD + 32 + 32 * HD + (size_t)(pos + 1)) * 4;
+        if (smem2 > 48 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(attn_decode2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                attr = true;
+            }
+        }
+        const cudaError_t e = launch_pdl(attn_decode2_kernel, dim3(H, E), dim3(ADT), smem2, (cudaStream_t)stream, qkv,
+                                         pos, d, H, kv, layer, L, T, out);
+        if (e != cudaSuccess) return set_error(DYQ_ECUDA, "attn_decode2_kernel: %s", cudaGetErrorString(e));
+        return check_launch("attn_decode2_kernel");
+    }
     const size_t smem = (HD + (size_t)(pos + 1) + 32 + 4 * HD) * 4;
     attn_decode_kernel<<<dim3(H, E), 256, smem, (cudaStream_t)stream>>>(qkv, pos, d, H, kv, layer, L, T, out);
     return check_launch("attn_decode_kernel");
