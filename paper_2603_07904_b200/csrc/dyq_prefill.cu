@@ -135,12 +135,18 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             for (int g = 0; g < NG; ++g) {
                 if (g >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
-                ptx::mbar_arrive_expect_tx(&full[s], cbytes + META_BLOCK + bbytes + PAR_BYTES);
-                ptx::bulk_g2s(st, a.codes + chunk_offset(L, tile, g * SPG, 0), cbytes, &full[s]);
-                ptx::bulk_g2s(st + a.off_meta, a.meta + meta_block(L, tile, g), META_BLOCK, &full[s]);
+                // (DYQ_EXP_NO_* : timing experiments only, tools/build_variant.py)
+#ifndef DYQ_EXP_MASK
+#define DYQ_EXP_MASK 0
+#endif
+                constexpr int XM = DYQ_EXP_MASK;  // bit 0 codes, 1 meta, 2 B, 3 s_x skipped
+                ptx::mbar_arrive_expect_tx(&full[s], (XM & 1 ? 0 : cbytes) + (XM & 2 ? 0 : META_BLOCK) +
+                                                         (XM & 4 ? 0 : bbytes) + (XM & 8 ? 0 : PAR_BYTES));
+                if (!(XM & 1)) ptx::bulk_g2s(st, a.codes + chunk_offset(L, tile, g * SPG, 0), cbytes, &full[s]);
+                if (!(XM & 2)) ptx::bulk_g2s(st + a.off_meta, a.meta + meta_block(L, tile, g), META_BLOCK, &full[s]);
                 const size_t tg = (size_t)tt * NG + g;
-                ptx::bulk_g2s(st + a.off_b, a.act + a.P.x16_off + tg * a.P.x16_group, bbytes, &full[s]);
-                ptx::bulk_g2s(st + a.off_par, a.act + a.P.par_off + tg * PAR_BYTES, PAR_BYTES, &full[s]);
+                if (!(XM & 4)) ptx::bulk_g2s(st + a.off_b, a.act + a.P.x16_off + tg * a.P.x16_group, bbytes, &full[s]);
+                if (!(XM & 8)) ptx::bulk_g2s(st + a.off_par, a.act + a.P.par_off + tg * PAR_BYTES, PAR_BYTES, &full[s]);
                 if (++s == S) { s = 0; ph ^= 1; }
             }
         }
@@ -151,9 +157,11 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
         uint32_t ph = 0, aph = 0;
         for (int g = 0; g < NG; ++g) {
             const int b = g & 1;
+            if (!(DYQ_EXP_MASK & 128)) {  // timing experiment: bit 7 = issue without waiting
             ptx::mbar_wait(&full[s], ph);      // B operand landed
             ptx::mbar_wait(&afull[ai], aph);   // A operand written to TMEM
             if (g >= 2) ptx::mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
+            }
             tc::fence_after();
             if (lane == 0) {
                 const uint32_t st = sbase + s * a.stage_bytes;
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 #pragma unroll
             for (int si = 0; si < 2; ++si) {
                 const int sub = 2 * q + si;
-                if (sub >= nsub) break;
+                if (sub >= nsub || (DYQ_EXP_MASK & 64)) break;
                 const uint32_t tl = at + ((uint32_t)(32 * q + 16 * si) << 16);
                 // zero points of rows gid and gid+8 are adjacent metadata slots
                 const uint32_t z01 = *reinterpret_cast<const uint16_t*>(zrow + sub * 16 + 2 * (lane >> 2));
@@ -320,6 +328,12 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                                     cf == 2 ? 0 : __float2int_rn(__uint_as_float(v[si * 4 * nblk + bi * 4 + j]));
                         }
             };
+            constexpr int XM2 = DYQ_EXP_MASK;  // timing experiments: bit 4 no promotion math, bit 5 no TMEM loads
+            if (XM2 & 32) {
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[b]);
+            } else {
 #pragma unroll
             for (int c = 0; c < 2; ++c) {  // blocks 0-3, 4-7
                 uint32_t v[32];
@@ -327,7 +341,8 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 tc::ld16x256_x4(tb + (16u << 16) + c * 32, v + 16);
                 tc::wait_ld();
                 if (PARTIALS) partials(v, 4, c * 4);
-                else promote(v, 4, c * 4);
+                else if (!(XM2 & 16)) promote(v, 4, c * 4);
+                else facc[c] += __uint_as_float(v[c]);
             }
             {  // block 8
                 uint32_t v[8];
@@ -338,7 +353,9 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&tempty[b]);
                 if (PARTIALS) partials(v, 1, 8);
-                else promote(v, 1, 8);
+                else if (!(XM2 & 16)) promote(v, 1, 8);
+                else facc[2] += __uint_as_float(v[2]);
+            }
             }
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&empty[s]);
