@@ -122,6 +122,8 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 // rotate_half RoPE on the q and k parts: pairs (i, i + HD/2) of every head
 __global__ void rope_kernel(uint16_t* __restrict__ qkv, int M, int S, int pos0, int d, int H, float theta) {
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int half = HD / 2;
     const size_t per_row = (size_t)2 * H * half;
@@ -581,6 +583,8 @@ __global__ void __launch_bounds__(ADT) attn_decode2_kernel(const uint16_t* __res
 }
 
 __global__ void silu_mul_kernel(const uint16_t* __restrict__ gu, int M, int ffn, uint16_t* __restrict__ act) {
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)M * ffn) return;
     const size_t m = idx / ffn, j = idx % ffn;
@@ -592,6 +596,8 @@ __global__ void silu_mul_kernel(const uint16_t* __restrict__ gu, int M, int ffn,
 __global__ void head_argmax_kernel(const uint16_t* __restrict__ x, int row_stride, int d,
                                    const uint16_t* __restrict__ W, int n_bins, float* __restrict__ logits,
                                    int32_t* __restrict__ tok, int tok_stride) {
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
     extern __shared__ __align__(16) float xs[];  // [d]
     __shared__ float bv[32];
     __shared__ int bi[32];
@@ -637,6 +643,8 @@ __global__ void head_argmax_kernel(const uint16_t* __restrict__ x, int row_strid
 __global__ void embed_prefill_kernel(const uint16_t* __restrict__ vis, const int32_t* __restrict__ text,
                                      const uint16_t* __restrict__ embed, int n_vis, int n_text, int d,
                                      uint16_t* __restrict__ h) {
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
     const int S = n_vis + n_text;
     const int row = blockIdx.x;  // e * S + i
     const int e = row / S, i = row % S;
@@ -649,6 +657,8 @@ __global__ void embed_prefill_kernel(const uint16_t* __restrict__ vis, const int
 // decode input: embedding of the previous action token (vocab id vocab - n_bins + bin)
 __global__ void embed_action_kernel(const int32_t* __restrict__ tok, int n_act, int t, const uint16_t* __restrict__ embed,
                                     int vocab, int n_bins, int d, uint16_t* __restrict__ h) {
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
     const int e = blockIdx.x;
     const int id = vocab - n_bins + tok[(size_t)e * n_act + t];
     for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8)
@@ -657,6 +667,8 @@ __global__ void embed_action_kernel(const int32_t* __restrict__ tok, int n_act, 
 
 __global__ void detok_kernel(const int32_t* __restrict__ tok, int E, int n_act, int n_bins, float* __restrict__ act,
                              float* __restrict__ prev, const int32_t* __restrict__ bits, int32_t* __restrict__ bits_out) {
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < E * n_act) {
         const float v = -1.f + (2.f * (float)tok[i] + 1.f) / (float)n_bins;
@@ -775,7 +787,9 @@ dyq_status_t dyq_rope(uint16_t* qkv, int32_t M, int32_t S, int32_t pos0, int32_t
     if (M < 0 || S <= 0 || d != H * HD) return set_error(DYQ_ESHAPE, "bad rope shape (head dim %d)", HD);
     if (M == 0) return DYQ_OK;
     const size_t n = (size_t)M * 2 * H * (HD / 2);
-    rope_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(qkv, M, S, pos0, d, H, theta);
+    const cudaError_t e = launch_pdl(rope_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
+                                     (cudaStream_t)stream, qkv, M, S, pos0, d, H, theta);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "rope_kernel: %s", cudaGetErrorString(e));
     return check_launch("rope_kernel");
 }
 
@@ -834,15 +848,18 @@ dyq_status_t dyq_silu_mul(const uint16_t* gu, int32_t M, int32_t ffn, uint16_t* 
     if (M < 0 || ffn <= 0) return set_error(DYQ_ESHAPE, "bad silu_mul shape");
     if (M == 0) return DYQ_OK;
     const size_t n = (size_t)M * ffn;
-    silu_mul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(gu, M, ffn, act);
+    const cudaError_t e = launch_pdl(silu_mul_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
+                                     (cudaStream_t)stream, gu, M, ffn, act);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "silu_mul_kernel: %s", cudaGetErrorString(e));
     return check_launch("silu_mul_kernel");
 }
 
 dyq_status_t dyq_head_argmax(const uint16_t* x, int32_t E, int32_t row_stride, int32_t d, const uint16_t* W,
                              int32_t n_bins, float* logits, int32_t* tok, int32_t tok_stride, dyq_stream_t stream) {
     if (E <= 0 || d <= 0 || d % 8 || n_bins <= 0) return set_error(DYQ_ESHAPE, "bad head shape");
-    head_argmax_kernel<<<E, 256, (size_t)d * 4, (cudaStream_t)stream>>>(x, row_stride, d, W, n_bins, logits, tok,
-                                                                          tok_stride);
+    const cudaError_t e = launch_pdl(head_argmax_kernel, dim3(E), dim3(256), (size_t)d * 4, (cudaStream_t)stream, x,
+                                     row_stride, d, W, n_bins, logits, tok, tok_stride);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "head_argmax_kernel: %s", cudaGetErrorString(e));
     return check_launch("head_argmax_kernel");
 }
 
@@ -956,21 +973,26 @@ dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t
     };
 
     // ---- prefill: vision + text tokens
-    embed_prefill_kernel<<<MP, 128, 0, st>>>(vis, text, D.embed, D.n_vis, D.n_text, d, h);
+    if (launch_pdl(embed_prefill_kernel, dim3(MP), dim3(128), 0, st, vis, text, D.embed, D.n_vis, D.n_text, d, h) !=
+        cudaSuccess)
+        return set_error(DYQ_ECUDA, "embed_prefill_kernel launch");
     DYQ_TRY(check_launch("embed_prefill_kernel"));
     DYQ_TRY(dyq_add_rmsnorm(h, nullptr, D.attn_norm, MP, d, D.rms_eps, xn, stream));
     for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, MP, rbp, true, 0));
     DYQ_TRY(dyq_head_argmax(xn + (size_t)(S - 1) * d, E, S, d, D.head_bins, D.n_bins, logits, tok, D.n_act, stream));
     // ---- decode passes: one action token per pass
     for (int t = 1; t < D.n_act; ++t) {
-        embed_action_kernel<<<E, 128, 0, st>>>(tok, D.n_act, t - 1, D.embed, D.vocab, D.n_bins, d, h);
+        if (launch_pdl(embed_action_kernel, dim3(E), dim3(128), 0, st, tok, D.n_act, t - 1, D.embed, D.vocab, D.n_bins,
+                       d, h) != cudaSuccess)
+            return set_error(DYQ_ECUDA, "embed_action_kernel launch");
         DYQ_TRY(check_launch("embed_action_kernel"));
         DYQ_TRY(dyq_add_rmsnorm(h, nullptr, D.attn_norm, E, d, D.rms_eps, xn, stream));
         for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, E, rbd, false, S + t - 1));
         DYQ_TRY(dyq_head_argmax(xn, E, 1, d, D.head_bins, D.n_bins, logits, tok + t, D.n_act, stream));
     }
-    detok_kernel<<<(E * D.n_act + 127) / 128, 128, 0, st>>>(tok, E, D.n_act, D.n_bins, action_out, prev, bits,
-                                                             bits_out);
+    if (launch_pdl(detok_kernel, dim3((E * D.n_act + 127) / 128), dim3(128), 0, st, tok, E, D.n_act, D.n_bins,
+                   action_out, prev, bits, bits_out) != cudaSuccess)
+        return set_error(DYQ_ECUDA, "detok_kernel launch");
     DYQ_TRY(check_launch("detok_kernel"));
 #undef DYQ_TRY
     m->t += 1;

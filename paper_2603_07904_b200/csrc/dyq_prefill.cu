@@ -96,6 +96,8 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
     uint8_t* s_col = smem + 512;  // per token column: 0 absent, 1 integer bits, 2 BF16 bypass
     uint8_t* stage0 = smem + 1024;
 
+    ptx::pdl_wait();  // the B operand, s_x and row_bits come from the preceding kernels
+    if (threadIdx.x == 0) ptx::pdl_launch_dependents();
     for (int i = threadIdx.x; i < PT; i += PRE_THREADS) {
         const int m = tt * PT + i;
         s_col[i] = m < a.M ? (token_bits(a, m) == 16 ? 2 : 1) : 0;
@@ -409,6 +411,8 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
                                     const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ act,
                                     PreActLayout P, int64_t* err) {
+    ptx::pdl_wait();  // x / row_bits come from the preceding kernels
+    ptx::pdl_launch_dependents();
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int NG = L.NG, G = L.G;
@@ -492,8 +496,18 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
     const PreActLayout P = pre_act_layout(L, M);
     const int TT = (M + PT - 1) / PT;
     const long long warps = (long long)TT * PT * L.NG;
-    actquant_pre_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
-        L, x, M, row_bits, bits, reinterpret_cast<uint8_t*>(act), P, err);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((warps * 32 + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, actquant_pre_kernel, L, x, M, row_bits, bits,
+                                             reinterpret_cast<uint8_t*>(act), P, err);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "actquant_pre_kernel launch: %s", cudaGetErrorString(e));
     return check_launch("actquant_pre_kernel");
 }
 
@@ -518,8 +532,17 @@ static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    kern<<<grid, PRE_THREADS, smem, st>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(PRE_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr1[1];
+    attr1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr1[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr1;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <bool PARTIALS>
