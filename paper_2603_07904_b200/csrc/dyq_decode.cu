@@ -652,18 +652,21 @@ static int env_int(const char* name, int dflt) {
 static DecPlan dec_plan(const WLayout& L, int nt8) {
     DecPlan p;
     const int unit_codes = (L.G / 64) * 8 * L.chunk;  // full tile
-    static const int stage_code_kb = env_int("DYQ_DEC_STAGE_KB", 32);
-    p.gps = (stage_code_kb * 1024) / unit_codes;
-    if (p.gps < 1) p.gps = 1;
-    if (p.gps > L.NG) p.gps = L.NG;
-    const int cps = nt8 * 8 * L.G + nt8 * 64, x16s = nt8 * 8 * L.G * 2;
-    p.off_meta = p.gps * unit_codes;
-    p.off_cp = p.off_meta + p.gps * META_BLOCK;
-    p.off_x16 = p.off_cp + p.gps * cps;
-    p.stage_bytes = p.off_x16 + p.gps * x16s;
+    // Stage code bytes: 64 KB measured best at M = 8 (B200: gate|up 15.9 us vs
+    // 16.9 us at 32 KB); halved until at least two stages fit the budget.
+    static const int stage_code_kb = env_int("DYQ_DEC_STAGE_KB", 64);
     static const int smem_kb1 = env_int("DYQ_DEC_SMEM_KB", 113);
     const int smem_kb = (nt8 == 1 && DEC_CWARPS == 8) ? smem_kb1 : 200;
-    p.stages = (smem_kb * 1024 - 256 - 16 * 1024) / p.stage_bytes;
+    const int cps = nt8 * 8 * L.G + nt8 * 64, x16s = nt8 * 8 * L.G * 2;
+    for (int want = (stage_code_kb * 1024) / unit_codes;; want /= 2) {
+        p.gps = want < 1 ? 1 : (want > L.NG ? L.NG : want);
+        p.off_meta = p.gps * unit_codes;
+        p.off_cp = p.off_meta + p.gps * META_BLOCK;
+        p.off_x16 = p.off_cp + p.gps * cps;
+        p.stage_bytes = p.off_x16 + p.gps * x16s;
+        p.stages = (smem_kb * 1024 - 256 - 16 * 1024) / p.stage_bytes;
+        if (p.stages >= 2 || p.gps == 1) break;
+    }
     p.stages = p.stages < 2 ? 2 : (p.stages > 8 ? 8 : p.stages);
     p.smem = 256 + (size_t)p.stages * p.stage_bytes + 8 * 32 * 8 * 4 + 8 * 1024;  // + combine + slot scratch
     const int U = L.T128 * L.NG;
