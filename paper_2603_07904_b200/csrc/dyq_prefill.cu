@@ -22,6 +22,12 @@
 // pipe's rate (half of i8) stays above what the promotion can consume.
 // BF16-bypass tokens (A16) use the same MMA with B = x and s_x = 1, so
 // one pass serves any mix of activation widths in a token tile.
+// E4M3 mode (W4 tiles whose tokens all run A2 / A4): every centred code
+// (|q - z_w| <= 15, |Xq - z_x| <= 15) is exact in e4m3 and the fp32 sums are
+// exact (tools/f8_probe.cu), so the same integer group sums come from
+// tcgen05.mma .kind::f8f6f4 with K = 32 per instruction -- half the MMAs and
+// half the B bytes of the bf16 path.  Decided per 144-token tile, identically
+// in the quantizer and here (dyq_pre_tile_e4m3).
 //
 // CTA = one 128-row weight tile x one 144-token tile (288 = 2 x 144: the OpenVLA
 // prefill of 256 vision + 32 text tokens tiles exactly), whole K, 14 warps:
@@ -39,6 +45,7 @@
 //               (FMUL2 + FFMA2) in registers; transposed 16-B stores at the end.
 // TMEM columns: [0,144) [144,288) accumulators, then NA A-operand buffers.
 #include <stdlib.h>
+#include <cuda_fp8.h>
 
 #include "dyq_internal.cuh"
 #include "dyq_ptx.cuh"
@@ -55,6 +62,7 @@ constexpr uint32_t ACC_COLS = 2 * PT;   // TMEM: two 144-column accumulators, th
 
 struct PreArgs {
     WLayout L;
+    int e4m3;  // e4m3 mode allowed (W4; DYQ_PRE_E4M3=0 disables)
     const uint8_t* codes;
     const uint8_t* meta;
     const int32_t* row_bits;
@@ -70,6 +78,14 @@ struct PreArgs {
 };
 
 __device__ __forceinline__ int token_bits(const PreArgs& a, int m) { return a.row_bits ? a.row_bits[m] : a.bits; }
+
+// Physical byte position, inside one 32-k e4m3 K step, of logical k (0..31):
+// the packed W4 fragment puts k = 4t + i (low nibbles) in TMEM column 2t and
+// k = 16 + 4t + i (high nibbles) in column 2t + 1, so B follows that order.
+__host__ __device__ inline int e4m3_kpos(int kl) { return 8 * ((kl >> 2) & 3) + 4 * ((kl >> 4) & 1) + (kl & 3); }
+__device__ __forceinline__ uint8_t e4m3_of(float v) {  // exact for integers |v| <= 15
+    return (uint8_t)__nv_cvt_float_to_fp8(v, __NV_SATFINITE, __NV_E4M3);
+}
 
 template <int WBITS, int SPG, bool PARTIALS>
 __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const PreArgs a) {
@@ -98,10 +114,15 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 
     ptx::pdl_wait();  // the B operand, s_x and row_bits come from the preceding kernels
     if (threadIdx.x == 0) ptx::pdl_launch_dependents();
+    int ok8 = 1;
     for (int i = threadIdx.x; i < PT; i += PRE_THREADS) {
         const int m = tt * PT + i;
-        s_col[i] = m < a.M ? (token_bits(a, m) == 16 ? 2 : 1) : 0;
+        const int bm = m < a.M ? token_bits(a, m) : 2;
+        s_col[i] = m < a.M ? (bm == 16 ? 2 : 1) : 0;
+        ok8 &= (bm == 2 || bm == 4);
     }
+    // tile mode (uniform per CTA; the quantizer decides identically)
+    const bool f8 = __syncthreads_and(ok8) && WBITS == 4 && a.e4m3;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -131,7 +152,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
         // ------------------------------------------------------ producer
         if (lane == 0) {
             const uint32_t cbytes = (uint32_t)(SPG * nsub * L.chunk);
-            const uint32_t bbytes = KSTEPS * BSTEP;
+            const uint32_t bbytes = f8 ? KSTEPS * BSTEP / 2 : KSTEPS * BSTEP;  // e4m3: K = 32 per step
             int s = 0;
             uint32_t ph = 0;
             for (int g = 0; g < NG; ++g) {
@@ -169,10 +190,19 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 const uint32_t st = sbase + s * a.stage_bytes;
                 const uint32_t d = tmem + b * PT;
                 const uint32_t at = tmem + ACC_COLS + ai * A_COLS;
+                if (f8) {
+                    constexpr uint32_t idesc8 = tc::idesc_e4m3(128, PT);
 #pragma unroll
-                for (int ks = 0; ks < KSTEPS; ++ks) {
-                    const uint64_t bd = tc::smem_desc(st + a.off_b + ks * BSTEP, 128, 256);
-                    tc::mma_f16_ta(d, at + ks * 8, bd, idesc, ks > 0);
+                    for (int ks = 0; ks < KSTEPS / 2; ++ks) {
+                        const uint64_t bd = tc::smem_desc(st + a.off_b + ks * BSTEP, 128, 256);
+                        tc::mma_f8_ta(d, at + ks * 8, bd, idesc8, ks > 0);
+                    }
+                } else {
+#pragma unroll
+                    for (int ks = 0; ks < KSTEPS; ++ks) {
+                        const uint64_t bd = tc::smem_desc(st + a.off_b + ks * BSTEP, 128, 256);
+                        tc::mma_f16_ta(d, at + ks * 8, bd, idesc, ks > 0);
+                    }
                 }
                 tc::commit(ptx::smem_u32(&tfull[b]));
                 tc::commit(ptx::smem_u32(&empty[s]));
@@ -206,7 +236,35 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 const uint32_t tl = at + ((uint32_t)(32 * q + 16 * si) << 16);
                 // zero points of rows gid and gid+8 are adjacent metadata slots
                 const uint32_t z01 = *reinterpret_cast<const uint16_t*>(zrow + sub * 16 + 2 * (lane >> 2));
-                if (WBITS == 4) {
+                if (WBITS == 4 && f8) {
+                    // e4m3 (q - z_w): K step = slab; TMEM column 2t <- low nibbles,
+                    // 2t + 1 <- high nibbles (e4m3_kpos), rows gid / gid + 8
+                    const float zf0 = 8388608.f + (float)(z01 & 0xffu), zf1 = 8388608.f + (float)(z01 >> 8);
+#pragma unroll
+                    for (int spi = 0; spi < SPG; ++spi) {
+                        const uint4 wv = *reinterpret_cast<const uint4*>(st + ((spi * nsub + sub) * 32 + lane) * 16);
+                        const uint32_t ws4[4] = {wv.x, wv.y, wv.z, wv.w};
+                        uint32_t r[8];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int slab = j >> 1, rs = j & 1;
+                            const float zf = rs ? zf1 : zf0;
+#pragma unroll
+                            for (int hn = 0; hn < 2; ++hn) {
+                                const uint32_t x = hn ? (ws4[j] >> 4) & 0x0F0F0F0Fu : ws4[j] & 0x0F0F0F0Fu;
+                                float v[4];
+#pragma unroll
+                                for (int bb = 0; bb < 4; ++bb)  // (2^23 + q) - (2^23 + z): exact q - z
+                                    v[bb] = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7540u + bb)) - zf;
+                                // two cvt.rn.satfinite.e4m3x2.f32 (low byte = first value)
+                                const uint32_t p01 = __nv_cvt_float2_to_fp8x2(make_float2(v[0], v[1]), __NV_SATFINITE, __NV_E4M3);
+                                const uint32_t p23 = __nv_cvt_float2_to_fp8x2(make_float2(v[2], v[3]), __NV_SATFINITE, __NV_E4M3);
+                                r[slab * 4 + rs * 2 + hn] = (p01 & 0xffffu) | (p23 << 16);
+                            }
+                        }
+                        tc::st16x256_x2(tl + spi * 16, r);
+                    }
+                } else if (WBITS == 4) {
                     // bf16 (128 + z) pairs; 0x43XX is exactly 128 + XX for XX < 128
                     const uint32_t zz0 = 0x43004300u | ((z01 & 0xffu) * 0x00010001u);
                     const uint32_t zz1 = 0x43004300u | ((z01 >> 8) * 0x00010001u);
@@ -410,7 +468,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 // (1 for A16 tokens, 0 for absent rows).
 __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
                                     const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ act,
-                                    PreActLayout P, int64_t* err) {
+                                    PreActLayout P, int64_t* err, int e4m3_ok) {
     ptx::pdl_wait();  // x / row_bits come from the preceding kernels
     ptx::pdl_launch_dependents();
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -424,7 +482,19 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
     const size_t tg = (size_t)tt * NG + g;
     const int m = tt * PT + row;
     const int b = m < M ? (row_bits ? row_bits[m] : bits) : 0;
+    // tile mode (dyq_pre_tile_e4m3): every present token of tile tt at A2 / A4
+    int ok8 = 1;
+    for (int i = lane; i < PT; i += 32) {
+        const int mm = tt * PT + i;
+        const int bm = mm < M ? (row_bits ? row_bits[mm] : bits) : 2;
+        ok8 &= (bm == 2 || bm == 4);
+    }
+    const bool f8 = __all_sync(0xffffffffu, ok8) && e4m3_ok;
     uint8_t* xg = act + P.x16_off + tg * P.x16_group;
+    auto x8_at = [&](int k) -> uint8_t* {  // e4m3 B operand: 32 k per K step, 32 B per row
+        const int ks = k >> 5, p = e4m3_kpos(k & 31);
+        return xg + ks * (PT * 32) + (row >> 3) * 256 + (p >> 4) * 128 + (row & 7) * 16 + (p & 15);
+    };
     auto x16_at = [&](int k) -> uint16_t* {
         const int ks = k >> 4, kk = k & 15;
         return reinterpret_cast<uint16_t*>(xg + ks * (PT * 32) + (row >> 3) * 256 + (kk >> 3) * 128 + (row & 7) * 16 +
@@ -457,7 +527,12 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
 #pragma unroll
         for (int i = 0; i < MAXV; ++i) {
             const int k = lane + 32 * i;
-            if (k < G) *x16_at(k) = (b == 16) ? raw[i] : (uint16_t)0;
+            if (k < G) {
+                if (f8)
+                    *x8_at(k) = 0;  // absent row (an f8 tile has no A16 rows)
+                else
+                    *x16_at(k) = (b == 16) ? raw[i] : (uint16_t)0;
+            }
         }
         if (lane == 0) *sxo = b == 16 ? 1.f : 0.f;
         return;
@@ -472,13 +547,26 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
         const int k = lane + 32 * i;
         if (k < G) {
             const int qv = quantize_one(v[i], s, z, b, L.round_mode);
-            *x16_at(k) = __bfloat16_as_ushort(__float2bfloat16_rn((float)(qv - z)));  // |qv - z| <= 255: exact
+            if (f8)
+                *x8_at(k) = e4m3_of((float)(qv - z));  // |qv - z| <= 15: exact in e4m3
+            else
+                *x16_at(k) = __bfloat16_as_ushort(__float2bfloat16_rn((float)(qv - z)));  // |qv - z| <= 255: exact
         }
     }
     if (lane == 0) *sxo = s;
 }
 
 // ------------------------------------------------------------------ host
+// e4m3 mode: W4 weights only (W8 centred codes reach +-255).  Off by default:
+// bit-exact, but its A-operand transform (cvt to e4m3) outweighs the halved MMA
+// count with 4 transform warps (B200: gate|up 137 vs 130 us);
+// DYQ_PRE_E4M3=1 enables it (read per call, so tests can exercise it).  Both
+// kernels of a call see the same value.
+static bool pre_e4m3_enabled(const WLayout& L) {
+    const char* v = getenv("DYQ_PRE_E4M3");
+    return v && atoi(v) != 0 && L.wbits == 4;
+}
+
 PreActLayout pre_act_layout(const WLayout& L, int M) {
     PreActLayout P;
     const int TT = (M + PT - 1) / PT;
@@ -506,7 +594,7 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, actquant_pre_kernel, L, x, M, row_bits, bits,
-                                             reinterpret_cast<uint8_t*>(act), P, err);
+                                             reinterpret_cast<uint8_t*>(act), P, err, pre_e4m3_enabled(L) ? 1 : 0);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "actquant_pre_kernel launch: %s", cudaGetErrorString(e));
     return check_launch("actquant_pre_kernel");
 }
@@ -566,6 +654,7 @@ dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* met
     a.I_out = I_out;
     a.act = reinterpret_cast<const uint8_t*>(act);
     a.P = pre_act_layout(L, M);
+    a.e4m3 = pre_e4m3_enabled(L) ? 1 : 0;
     const dim3 grid(L.T128, (M + PT - 1) / PT);
     const cudaError_t e = I_out ? pre_dispatch<true>(a, grid, st) : pre_dispatch<false>(a, grid, st);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "qlinear_prefill_kernel launch: %s", cudaGetErrorString(e));

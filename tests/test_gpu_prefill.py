@@ -146,3 +146,49 @@ def test_prefill_extreme_codes_exact(wbits, abits, G):
     y = torch.zeros(M, N, dtype=torch.float32, device=DEV)
     dyq.qlinear(wd, codes, meta, t_u16(x), M, torch.from_numpy(rb).to(DEV), 0, y, 0, ws)
     check_close(y.cpu().numpy(), yref, 1e-3)
+
+
+# ------------------------------------------------------- e4m3 prefill mode
+@pytest.fixture
+def e4m3_mode(monkeypatch):
+    """The opt-in kind::f8f6f4 path (DYQ_PRE_E4M3=1, read per call): W4 token
+    tiles whose tokens all run A2 / A4 use e4m3 centred codes."""
+    monkeypatch.setenv("DYQ_PRE_E4M3", "1")
+    yield
+
+
+@pytest.mark.parametrize("M,N,K,G", [(144, 272, 256, 64), (288, 128, 512, 64), (200, 144, 256, 128), (17, 128, 64, 64)])
+@pytest.mark.parametrize("mode", [2, 4, "mix24", "mixed"])
+def test_prefill_e4m3_partials_bit_exact(e4m3_mode, M, N, K, G, mode):
+    w = synth.weights_bf16(N, K, seed=11 * N + K)
+    x = synth.activations_bf16(M, K, seed=13 * M + K)
+    rb = np.array([(2, 4)[(i // 5) % 2] for i in range(M)], np.int32) if mode == "mix24" else _rb(M, mode)
+    pk = oracle.pack_weights(w, G, 4)
+    yref, Iref = oracle.qlinear(x, pk, G, rb, want_I=True)
+    wd, codes, meta = gpu_pack(w, G, 4)
+    ws = _ws(wd, M)
+    I = torch.full((M, N, K // G), -7, dtype=torch.int32, device=DEV)
+    dyq.qlinear_i32_partials(wd, codes, meta, t_u16(x), M, torch.from_numpy(rb).to(DEV), 0, I, ws)
+    got = I.cpu().numpy()
+    assert np.array_equal(got, Iref), f"{(got != Iref).sum()} mismatches"
+    y = torch.zeros(M, N, dtype=torch.float32, device=DEV)
+    dyq.qlinear(wd, codes, meta, t_u16(x), M, torch.from_numpy(rb).to(DEV), 0, y, 0, ws)
+    check_close(y.cpu().numpy(), yref, 1e-3)
+
+
+@pytest.mark.parametrize("abits", [2, 4])
+@pytest.mark.parametrize("G", [64, 128])
+def test_prefill_e4m3_extreme_codes_exact(e4m3_mode, abits, G):
+    """Extreme centred codes (|q - z_w| = 15, |Xq - z_x| = 2^ba - 1) through e4m3."""
+    M, N, K = 160, 256, 512
+    rng = np.random.default_rng(100 + G + abits)
+    w = _extreme(N, K, G, rng)
+    x = _extreme(M, K, G, rng)
+    rb = _rb(M, abits)
+    pk = oracle.pack_weights(w, G, 4)
+    _, Iref = oracle.qlinear(x, pk, G, rb, want_I=True)
+    wd, codes, meta = gpu_pack(w, G, 4)
+    ws = _ws(wd, M)
+    I = torch.full((M, N, K // G), -7, dtype=torch.int32, device=DEV)
+    dyq.qlinear_i32_partials(wd, codes, meta, t_u16(x), M, torch.from_numpy(rb).to(DEV), 0, I, ws)
+    assert np.array_equal(I.cpu().numpy(), Iref)
