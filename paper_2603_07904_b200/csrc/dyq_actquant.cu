@@ -12,7 +12,7 @@ namespace dyq {
 // in x16; padding rows (m >= M): all zero.
 __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, int M, int m0,
                                     const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ ws,
-                                    ActLayoutDec A, int64_t* err, uint64_t* trace, uint32_t serial) {
+                                    ActLayoutDec A, int64_t* err, uint64_t* trace, uint32_t serial, int gated) {
     ptx::pdl_launch_dependents();
     if (threadIdx.x == 0) trace_ev(trace, serial, 2, 0);
     ptx::pdl_wait();  // x may be produced by the preceding kernel
@@ -29,7 +29,9 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
     uint8_t* zdst = ws + A.zx_off + (size_t)g * DEC_MPAD + m;
     const int b = (m < M) ? (row_bits ? row_bits[m0 + m] : bits) : 0;
     const bool centred = dec_call_centred(M, m0, row_bits, bits);
-    const uint16_t* src = x + (size_t)(m0 + m) * L.K + (size_t)g * L.G;
+    // gated: x = [g | u] rows of width 2K (SwiGLU input); the activation is
+    // bf16(silu(g) * u), the same float ops as silu_mul_kernel (dyq_model.cu)
+    const uint16_t* src = x + (size_t)(m0 + m) * L.K * (gated ? 2 : 1) + (size_t)g * L.G;
     constexpr int MAXV = 4;  // G <= 128
     float v[MAXV];
     uint16_t raw[MAXV];
@@ -41,7 +43,7 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
         v[i] = 0.f;
         raw[i] = 0;
         if (k < L.G && b != 0) {
-            raw[i] = src[k];
+            raw[i] = gated ? silu_mul_bf16(src[k], src[k + L.K]) : src[k];
             v[i] = bf16_bits_to_float(raw[i]);
             if (!finite_f(v[i])) bad = min(bad, k);
             vmin = fminf(vmin, v[i]);
@@ -94,7 +96,7 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
 }
 
 dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int m0, const int32_t* row_bits,
-                                 int bits, void* ws, int64_t* err, cudaStream_t st) {
+                                 int bits, void* ws, int64_t* err, cudaStream_t st, int gated) {
     // rows m0 .. m0+M-1 (M <= DEC_MPAD) of x / row_bits (base pointers)
     const ActLayoutDec A = act_layout_dec(L, dec_nt8(M));
     const int warps = 8 * A.nt8 * L.NG;
@@ -108,7 +110,7 @@ dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, actquant_dec_kernel, L, x, M, m0, row_bits, bits,
-                                             reinterpret_cast<uint8_t*>(ws), A, err, g_trace, g_trace_serial++);
+                                             reinterpret_cast<uint8_t*>(ws), A, err, g_trace, g_trace_serial++, gated);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "actquant_dec_kernel launch: %s", cudaGetErrorString(e));
     return check_launch("actquant_dec_kernel");
 }

@@ -269,24 +269,43 @@ static dyq_status_t validate_ql(const dyq_wdesc_t* wd, WLayout* L, const void* c
 // (programmatic dependent launch lets it start before the quantizer ends).
 static dyq_status_t run_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int32_t M,
                                const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype, int32_t* I, void* ws,
-                               int64_t* err, cudaStream_t st) {
+                               int64_t* err, cudaStream_t st, int gated = 0) {
     if (g_path == 2 || (g_path == 0 && M > DEC_MPAD)) {
         // prefill: tcgen05 kernels over 128-token tiles
         uint8_t* pa = reinterpret_cast<uint8_t*>(ws) + prefill_area_offset(L);
-        dyq_status_t rc = launch_actquant_pre(L, x, M, row_bits, bits, pa, err, st);
+        dyq_status_t rc = launch_actquant_pre(L, x, M, row_bits, bits, pa, err, st, gated);
         if (rc) return rc;
         return launch_prefill(L, codes, meta, M, row_bits, bits, y, y_dtype, I, pa, st);
     }
     uint8_t* area = reinterpret_cast<uint8_t*>(ws) + act_area_offset(L);
     for (int m0 = 0; m0 < M; m0 += DEC_MPAD) {
         const int mt = (M - m0) < DEC_MPAD ? (M - m0) : DEC_MPAD;
-        dyq_status_t rc = launch_actquant_dec(L, x, mt, m0, row_bits, bits, area, err, st);
+        dyq_status_t rc = launch_actquant_dec(L, x, mt, m0, row_bits, bits, area, err, st, gated);
         if (rc) return rc;
         rc = launch_decode(L, codes, meta, x, mt, m0, row_bits, bits, y, y_dtype, I, ws, err, st);
         if (rc) return rc;
     }
     return DYQ_OK;
 }
+
+}  // extern "C"
+
+namespace dyq {
+// Policy-step internal (not exported): dyq_qlinear on the SwiGLU activation of
+// gu = [g | u] (rows of 2K); the quantizers form bf16(silu(g) u) on the fly,
+// bit-identical to dyq_silu_mul followed by dyq_qlinear.
+dyq_status_t qlinear_gated(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* gu, int32_t M,
+                           const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype, void* ws, size_t ws_bytes,
+                           int64_t* err, cudaStream_t st) {
+    WLayout L;
+    dyq_status_t rc = validate_ql(wd, &L, codes, meta, gu, M, row_bits, bits, y != nullptr, y_dtype, true, ws,
+                                  ws_bytes);
+    if (rc || M == 0) return rc;
+    return run_decode(L, codes, meta, gu, M, row_bits, bits, y, y_dtype, nullptr, ws, err, st, 1);
+}
+}  // namespace dyq
+
+extern "C" {
 
 dyq_status_t dyq_qlinear(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x, int32_t M,
                          const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype, void* workspace,

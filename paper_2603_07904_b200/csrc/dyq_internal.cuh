@@ -186,6 +186,14 @@ __device__ inline int quantize_one(float v, float s, int z, int bits, int round_
 
 __device__ inline bool finite_f(float v) { return isfinite(v); }
 
+// SwiGLU activation of one element, bf16(silu(g) * u) with fp32 math -- the
+// exact float ops of silu_mul_kernel (dyq_model.cu), so the fused and the
+// separate path give identical bits.
+__device__ __forceinline__ uint16_t silu_mul_bf16(uint16_t gb, uint16_t ub) {
+    const float g = bf16_bits_to_float(gb), u = bf16_bits_to_float(ub);
+    return __bfloat16_as_ushort(__float2bfloat16_rn(g / (1.f + __expf(-g)) * u));
+}
+
 // -------------------------------------------------------------- warp ops
 __device__ inline float warp_min(float v) {
 #pragma unroll
@@ -207,7 +215,7 @@ size_t decode_ws_bytes(const WLayout& L);
 dyq_status_t launch_prefetch_l2(const void* p, size_t bytes, cudaStream_t st);
 PreActLayout pre_act_layout(const WLayout& L, int M);
 dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, const int32_t* row_bits, int bits,
-                                 void* act, int64_t* err, cudaStream_t st);
+                                 void* act, int64_t* err, cudaStream_t st, int gated = 0);
 dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,
                             int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st);
 extern int g_path;
@@ -235,7 +243,12 @@ dyq_status_t launch_pack(const WLayout& L, const uint16_t* w, void* codes, void*
 dyq_status_t launch_unpack(const WLayout& L, const void* codes, const void* meta, uint8_t* q,
                            float* s, uint8_t* z, cudaStream_t st);
 dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int m0, const int32_t* row_bits,
-                                 int bits, void* ws, int64_t* err, cudaStream_t st);
+                                 int bits, void* ws, int64_t* err, cudaStream_t st, int gated = 0);
+// dyq_qlinear on the SwiGLU of gu = [g | u] (rows of 2K): the activation
+// quantizers form bf16(silu(g) * u) on the fly (policy step, not exported).
+dyq_status_t qlinear_gated(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* gu, int32_t M,
+                           const int32_t* row_bits, int32_t bits, void* y, int32_t y_dtype, void* ws, size_t ws_bytes,
+                           int64_t* err, cudaStream_t st);
 dyq_status_t launch_actquant_export(const WLayout& L, int M, const int32_t* row_bits, int bits, const void* ws,
                                     uint8_t* xq, float* sx, uint8_t* zx, int32_t* SX, int m0, cudaStream_t st);
 // rows m0 .. m0+M-1 (M <= DEC_MPAD); x, row_bits, y, I_out are base pointers;
@@ -243,20 +256,4 @@ dyq_status_t launch_actquant_export(const WLayout& L, int M, const int32_t* row_
 dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int M,
                            int m0, const int32_t* row_bits, int bits, void* y, int y_dtype, int32_t* I_out,
                            void* ws, int64_t* err, cudaStream_t st);
-size_t decode_ws_bytes(const WLayout& L);
-PreActLayout pre_act_layout(const WLayout& L, int M);
-dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, const int32_t* row_bits, int bits,
-                                 void* act, int64_t* err, cudaStream_t st);
-dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,
-                            int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st);
-extern int g_path;
-// dyq_select.cu
-size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
-dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);
-dyq_status_t launch_sel_reset(void* state, int32_t E, const uint8_t* mask, cudaStream_t st);
-dyq_status_t launch_select(void* state, int32_t E, const dyq_calib_t* cal_or_null, const float* prev_action,
-                           int32_t* bits, double* S_out, int32_t* target_out, int32_t tpe, const int32_t* tab4,
-                           int32_t* row_bits, cudaStream_t st);
-dyq_status_t launch_route(const int32_t* bits, int32_t E, int32_t tpe, const int32_t* tab4, int32_t* row_bits,
-                          cudaStream_t st);
 }  // namespace dyq

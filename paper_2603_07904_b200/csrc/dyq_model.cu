@@ -964,9 +964,10 @@ dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t
         DYQ_TRY(dyq_add_rmsnorm(h, delta, D.mlp_norm + (size_t)l * d, M, d, D.rms_eps, xn, stream));
         DYQ_TRY(dyq_qlinear(&wd[2], m->codes[li + 2], m->meta[li + 2], xn, M, rb, 0, gu, 1, ws[2], L.ws_bytes[2],
                             err, stream));
-        DYQ_TRY(dyq_silu_mul(gu, M, ffn, act, stream));
-        DYQ_TRY(dyq_qlinear(&wd[3], m->codes[li + 3], m->meta[li + 3], act, M, rb, 0, delta, 1, ws[3], L.ws_bytes[3],
-                            err, stream));
+        // SwiGLU fused into the down projection's activation quantization
+        // (bit-identical to dyq_silu_mul + dyq_qlinear; one launch less per layer)
+        DYQ_TRY(qlinear_gated(&wd[3], m->codes[li + 3], m->meta[li + 3], gu, M, rb, 0, delta, 1, ws[3], L.ws_bytes[3],
+                              err, st));
         const uint16_t* nw = l + 1 < NL ? D.attn_norm + (size_t)(l + 1) * d : D.final_norm;
         DYQ_TRY(dyq_add_rmsnorm(h, delta, nw, M, d, D.rms_eps, xn, stream));
         return DYQ_OK;

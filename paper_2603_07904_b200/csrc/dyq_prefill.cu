@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 // (1 for A16 tokens, 0 for absent rows).
 __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
                                     const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ act,
-                                    PreActLayout P, int64_t* err, int e4m3_ok) {
+                                    PreActLayout P, int64_t* err, int e4m3_ok, int gated) {
     ptx::pdl_wait();  // x / row_bits come from the preceding kernels
     ptx::pdl_launch_dependents();
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -501,7 +501,7 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
                                            (kk & 7) * 2);
     };
     float* sxo = reinterpret_cast<float*>(act + P.par_off + tg * PAR_BYTES) + row;
-    const uint16_t* src = x + (size_t)m * L.K + (size_t)g * G;
+    const uint16_t* src = x + (size_t)m * L.K * (gated ? 2 : 1) + (size_t)g * G;  // gated: [g | u] rows
     constexpr int MAXV = 4;
     float v[MAXV];
     uint16_t raw[MAXV];
@@ -513,7 +513,7 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
         raw[i] = 0;
         v[i] = 0.f;
         if (k < G && b != 0) {
-            raw[i] = src[k];
+            raw[i] = gated ? silu_mul_bf16(src[k], src[k + L.K]) : src[k];
             v[i] = bf16_bits_to_float(raw[i]);
             if (!finite_f(v[i])) bad = min(bad, k);
             vmin = fminf(vmin, v[i]);
@@ -580,7 +580,7 @@ PreActLayout pre_act_layout(const WLayout& L, int M) {
 }
 
 dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, const int32_t* row_bits, int bits,
-                                 void* act, int64_t* err, cudaStream_t st) {
+                                 void* act, int64_t* err, cudaStream_t st, int gated) {
     const PreActLayout P = pre_act_layout(L, M);
     const int TT = (M + PT - 1) / PT;
     const long long warps = (long long)TT * PT * L.NG;
@@ -594,7 +594,7 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, actquant_pre_kernel, L, x, M, row_bits, bits,
-                                             reinterpret_cast<uint8_t*>(act), P, err, pre_e4m3_enabled(L) ? 1 : 0);
+                                             reinterpret_cast<uint8_t*>(act), P, err, pre_e4m3_enabled(L) ? 1 : 0, gated);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "actquant_pre_kernel launch: %s", cudaGetErrorString(e));
     return check_launch("actquant_pre_kernel");
 }
