@@ -321,3 +321,50 @@ def test_route_bits_variant_table():
     assert rb.cpu().numpy().tolist() == [2] * 3 + [4] * 3 + [8] * 3 + [16] * 3
     dyq.route_bits(bits, 4, 3, rb, abits_of=(4, 4, 8, 16))
     assert rb.cpu().numpy().tolist() == [4] * 6 + [8] * 3 + [16] * 3
+
+
+# ------------------------------------------------- hint / debug entry points
+def test_prefetch_l2_is_a_pure_hint():
+    """dyq_prefetch_l2 only moves bytes into L2: results are unchanged, and a
+    null / misaligned pointer is rejected synchronously."""
+    N, K, G, M = 512, 1024, 64, 8
+    w = synth.weights_bf16(N, K, seed=71)
+    x = synth.activations_bf16(M, K, seed=72)
+    wd, codes, meta = gpu_pack(w, G, 4)
+    ws = torch.zeros(max(16, dyq.qlinear_workspace(wd, M)), dtype=torch.uint8, device=DEV)
+    y0 = torch.zeros(M, N, dtype=torch.float32, device=DEV)
+    y1 = torch.zeros_like(y0)
+    dyq.qlinear(wd, codes, meta, t_u16(x), M, None, 4, y0, 0, ws)
+    dyq.prefetch_l2(codes)
+    dyq.prefetch_l2(meta)
+    dyq.qlinear(wd, codes, meta, t_u16(x), M, None, 4, y1, 0, ws)
+    assert torch.equal(y0, y1)
+    with pytest.raises(dyq.DyqError):
+        dyq._call("dyq_prefetch_l2", dyq.C.c_void_p(codes.data_ptr() + 1), 64, dyq._stream(None))
+
+
+def test_trace_records_decode_events():
+    """dyq_trace_enable: every decode CTA logs start / data / end events with
+    non-decreasing timestamps per CTA; disabling stops recording."""
+    N, K, G, M = 2048, 1024, 64, 8
+    w = synth.weights_bf16(N, K, seed=73)
+    x = synth.activations_bf16(M, K, seed=74)
+    wd, codes, meta = gpu_pack(w, G, 4)
+    ws = torch.zeros(max(16, dyq.qlinear_workspace(wd, M)), dtype=torch.uint8, device=DEV)
+    y = torch.zeros(M, N, dtype=torch.float32, device=DEV)
+    tr = torch.zeros(1 << 16, dtype=torch.int64, device=DEV)
+    dyq.trace_enable(tr)
+    dyq.qlinear(wd, codes, meta, t_u16(x), M, None, 4, y, 0, ws)
+    torch.cuda.synchronize()
+    dyq.trace_enable(None)
+    ev = [e for e in dyq.trace_read(tr) if e[1] == 1]  # kernel id 1 = decode
+    assert ev, "no decode events recorded"
+    by_cta = {}
+    for ser, k, e, b, t in ev:
+        by_cta.setdefault(b, {})[e] = t
+    for b, d in by_cta.items():
+        assert 0 in d and 4 in d and d[0] <= d[4]
+    n = int(tr[0].item())
+    dyq.qlinear(wd, codes, meta, t_u16(x), M, None, 4, y, 0, ws)
+    torch.cuda.synchronize()
+    assert int(tr[0].item()) == n  # disabled: nothing more recorded
