@@ -62,7 +62,8 @@ constexpr uint32_t ACC_COLS = 2 * PT;   // TMEM: two 144-column accumulators, th
 
 struct PreArgs {
     WLayout L;
-    int e4m3;  // e4m3 mode allowed (W4; DYQ_PRE_E4M3=0 disables)
+    int e4m3;  // e4m3 mode allowed (W4; DYQ_PRE_E4M3=1 enables)
+    uint64_t* trace;  // dyq_trace_enable buffer: per-group events of CTA (0,0), or null
     const uint8_t* codes;
     const uint8_t* meta;
     const int32_t* row_bits;
@@ -110,6 +111,16 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
     uint64_t* aempty = afull + NA; // [NA]
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(aempty + NA);
     uint8_t* s_col = smem + 512;  // per token column: 0 absent, 1 integer bits, 2 BF16 bypass
+    // per-group event ev of CTA (0,0): a plain store at trace[16 + 512 ev + g]
+    // (no atomics: tracing adds no latency to the pipeline it observes)
+    uint64_t* const tr = (blockIdx.x == 0 && blockIdx.y == 0) ? a.trace : nullptr;
+    auto tev = [&](uint32_t ev, int g) {
+        if (tr && g < 512) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            tr[16 + 512 * ev + g] = t;
+        }
+    };
     uint8_t* stage0 = smem + 1024;
 
     ptx::pdl_wait();  // the B operand, s_x and row_bits come from the preceding kernels
@@ -170,6 +181,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 const size_t tg = (size_t)tt * NG + g;
                 if (!(XM & 4)) ptx::bulk_g2s(st + a.off_b, a.act + a.P.x16_off + tg * a.P.x16_group, bbytes, &full[s]);
                 if (!(XM & 8)) ptx::bulk_g2s(st + a.off_par, a.act + a.P.par_off + tg * PAR_BYTES, PAR_BYTES, &full[s]);
+                tev(1, g);
                 if (++s == S) { s = 0; ph ^= 1; }
             }
         }
@@ -182,8 +194,11 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             const int b = g & 1;
             if (!(DYQ_EXP_MASK & 128)) {  // timing experiment: bit 7 = issue without waiting
             ptx::mbar_wait(&full[s], ph);      // B operand landed
+            if (lane == 0) tev(2, g);
             ptx::mbar_wait(&afull[ai], aph);   // A operand written to TMEM
+            if (lane == 0) tev(3, g);
             if (g >= 2) ptx::mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
+            if (lane == 0) tev(4, g);
             }
             tc::fence_after();
             if (lane == 0) {
@@ -328,6 +343,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             if (lane == 0) {
                 ptx::mbar_arrive(&afull[ai]);
                 ptx::mbar_arrive(&empty[s]);
+                if (warp == 2) tev(5, g);
             }
             if (++s == S) { s = 0; ph ^= 1; }
             if (++ai == NA) { ai = 0; aph ^= 1; }
@@ -349,6 +365,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
         for (int g = 0; g < NG; ++g) {
             const int b = g & 1;
             ptx::mbar_wait(&tfull[b], (g >> 1) & 1);
+            if (warp == PR_WARP0 && lane == 0) tev(6, g);
             tc::fence_after();
             const uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
             const float* swp = reinterpret_cast<const float*>(st + a.off_meta);
@@ -419,6 +436,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             }
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            if (warp == PR_WARP0 && lane == 0) tev(7, g);
             if (++s == S) s = 0;
         }
         if constexpr (!PARTIALS) {
@@ -655,6 +673,7 @@ dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* met
     a.act = reinterpret_cast<const uint8_t*>(act);
     a.P = pre_act_layout(L, M);
     a.e4m3 = pre_e4m3_enabled(L) ? 1 : 0;
+    a.trace = g_trace;
     const dim3 grid(L.T128, (M + PT - 1) / PT);
     const cudaError_t e = I_out ? pre_dispatch<true>(a, grid, st) : pre_dispatch<false>(a, grid, st);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "qlinear_prefill_kernel launch: %s", cudaGetErrorString(e));
