@@ -579,11 +579,52 @@ def main():
             y_host.copy_(ys[-1], non_blocking=True)
             b_host.copy_(bits, non_blocking=True)
             torch.cuda.current_stream().synchronize()
+        dt_eager = episodes.max_over_ranks((time.perf_counter() - tc) / n_e2e, device=dev)
+        # the same public-API step captured as a CUDA graph, one per step index
+        # k = t % 8 (input set k from its pinned buffers, weight copy k % C):
+        # pinned H2D of the step's inputs, select_route, 4 x dyq_qlinear, D2H of
+        # y and b*.  Per step the host writes a_{t-1} into a pinned staging
+        # buffer (28 B), replays graph t % 8 and waits for the result.
+        assert 8 % C == 0 or C % 8 == 0
+        a_stage = torch.empty(1, 7, dtype=torch.float32).pin_memory()
+        se = torch.cuda.Stream()
+        graphs = []
+        for k in range(8):
+            ge = torch.cuda.CUDAGraph()
+            se.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(ge, stream=se):
+                a_dev.copy_(a_stage, non_blocking=True)
+                for li in range(len(lins)):
+                    x_dev[li].copy_(x_host[k][li], non_blocking=True)
+                dyq.select_route(state, 1, a_dev, bits, M, row_bits, stream=se)
+                for li, (name, N, K) in enumerate(lins):
+                    p = packed[k % C][li]
+                    dyq.qlinear(p.wd, p.codes, p.meta, x_dev[li], M, row_bits, 0, ys[li], 1, wss[li], stream=se)
+                y_host.copy_(ys[-1], non_blocking=True)
+                b_host.copy_(bits, non_blocking=True)
+            graphs.append(ge)
+        torch.cuda.synchronize()
+        t_e = t_cur + args.steps + n_e2e
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        tc = time.perf_counter()
+        for i in range(n_e2e):
+            t = t_e + i
+            a_stage.copy_(a_host[t - 1])
+            graphs[t % 8].replay()  # enqueued on the current stream
+            torch.cuda.current_stream().synchronize()
         dt = episodes.max_over_ranks((time.perf_counter() - tc) / n_e2e, device=dev)
+        del graphs
         e2e = {"value": round(bytes_step * world / dt / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(dt * 1e3, 4), "steps": n_e2e,
-               "path": "eager dyq_* calls via the Python binding, pinned H2D in, D2H out, sync per step"}
+               "path": "public API (select_route + 4 x dyq_qlinear) captured per step index in a CUDA graph with "
+                       "the pinned H2D input copies and the D2H of y and b*; per step: host writes a_{t-1} into a "
+                       "pinned staging buffer, graph replay, stream sync",
+               "eager": {"value": round(bytes_step * world / dt_eager / 1e9, 2),
+                         "ms_per_step": round(dt_eager * 1e3, 4),
+                         "path": "eager dyq_* calls via the Python binding, pinned H2D in, D2H out, sync per step"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
