@@ -654,6 +654,83 @@ __global__ void embed_prefill_kernel(const uint16_t* __restrict__ vis, const int
         *reinterpret_cast<uint4*>(h + (size_t)row * d + c) = *reinterpret_cast<const uint4*>(src + c);
 }
 
+// Action head, spread over many CTAs: CTA (e, bin block) computes 32 bins'
+// logits with one warp per bin (coalesced 16-B loads of W rows, warp-shuffle
+// sums); the argmax over the logits row is a second tiny kernel (lowest index
+// among equal maxima, as head_argmax_kernel).
+constexpr int HB = 32;  // bins per CTA
+__global__ void __launch_bounds__(256) head_logits_kernel(const uint16_t* __restrict__ x, int row_stride, int d,
+                                                          const uint16_t* __restrict__ W, int n_bins,
+                                                          float* __restrict__ logits) {
+    extern __shared__ __align__(16) float xsh[];  // [d]
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    const int e = blockIdx.x, b0 = blockIdx.y * HB;
+    const uint16_t* xr = x + (size_t)e * row_stride * d;
+    for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(xr + i);
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            xsh[i + 2 * u] = __uint_as_float(vv[u] << 16);
+            xsh[i + 2 * u + 1] = __uint_as_float(vv[u] & 0xffff0000u);
+        }
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int bb = warp; bb < HB; bb += 8) {
+        const int b = b0 + bb;
+        if (b >= n_bins) break;
+        const uint16_t* wr = W + (size_t)b * d;
+        float s = 0.f;
+        for (int i = lane * 8; i < d; i += 256) {
+            const uint4 w8 = *reinterpret_cast<const uint4*>(wr + i);
+            const float4 xa = *reinterpret_cast<const float4*>(xsh + i);
+            const float4 xb = *reinterpret_cast<const float4*>(xsh + i + 4);
+            s = fmaf(xa.x, __uint_as_float(w8.x << 16), s);
+            s = fmaf(xa.y, __uint_as_float(w8.x & 0xffff0000u), s);
+            s = fmaf(xa.z, __uint_as_float(w8.y << 16), s);
+            s = fmaf(xa.w, __uint_as_float(w8.y & 0xffff0000u), s);
+            s = fmaf(xb.x, __uint_as_float(w8.z << 16), s);
+            s = fmaf(xb.y, __uint_as_float(w8.z & 0xffff0000u), s);
+            s = fmaf(xb.z, __uint_as_float(w8.w << 16), s);
+            s = fmaf(xb.w, __uint_as_float(w8.w & 0xffff0000u), s);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) logits[(size_t)e * n_bins + b] = s;
+    }
+}
+__global__ void __launch_bounds__(256) argmax_rows_kernel(const float* __restrict__ logits, int n_bins,
+                                                          int32_t* __restrict__ tok, int tok_stride) {
+    __shared__ float bv[32];
+    __shared__ int bi[32];
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    const int e = blockIdx.x;
+    float best = -INFINITY;
+    int bidx = 0x7fffffff;
+    for (int b = threadIdx.x; b < n_bins; b += blockDim.x) {
+        const float s = logits[(size_t)e * n_bins + b];
+        if (s > best || (s == best && b < bidx)) { best = s; bidx = b; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+        if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = bidx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        best = bv[0];
+        bidx = bi[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (bv[w] > best || (bv[w] == best && bi[w] < bidx)) { best = bv[w]; bidx = bi[w]; }
+        tok[(size_t)e * tok_stride] = bidx;
+    }
+}
+
 // decode input: embedding of the previous action token (vocab id vocab - n_bins + bin)
 __global__ void embed_action_kernel(const int32_t* __restrict__ tok, int n_act, int t, const uint16_t* __restrict__ embed,
                                     int vocab, int n_bins, int d, uint16_t* __restrict__ h) {
@@ -857,6 +934,15 @@ dyq_status_t dyq_silu_mul(const uint16_t* gu, int32_t M, int32_t ffn, uint16_t* 
 dyq_status_t dyq_head_argmax(const uint16_t* x, int32_t E, int32_t row_stride, int32_t d, const uint16_t* W,
                              int32_t n_bins, float* logits, int32_t* tok, int32_t tok_stride, dyq_stream_t stream) {
     if (E <= 0 || d <= 0 || d % 8 || n_bins <= 0) return set_error(DYQ_ESHAPE, "bad head shape");
+    if (logits && d % 256 == 0 && ((uintptr_t)x | (uintptr_t)W) % 16 == 0 && (size_t)d * 4 <= 48 * 1024) {
+        cudaError_t e = launch_pdl(head_logits_kernel, dim3(E, (n_bins + HB - 1) / HB), dim3(256), (size_t)d * 4,
+                                   (cudaStream_t)stream, x, row_stride, d, W, n_bins, logits);
+        if (e == cudaSuccess)
+            e = launch_pdl(argmax_rows_kernel, dim3(E), dim3(256), 0, (cudaStream_t)stream, (const float*)logits, n_bins,
+                           tok, tok_stride);
+        if (e != cudaSuccess) return set_error(DYQ_ECUDA, "head_logits/argmax: %s", cudaGetErrorString(e));
+        return check_launch("head_logits_kernel");
+    }
     const cudaError_t e = launch_pdl(head_argmax_kernel, dim3(E), dim3(256), (size_t)d * 4, (cudaStream_t)stream, x,
                                      row_stride, d, W, n_bins, logits, tok, tok_stride);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "head_argmax_kernel: %s", cudaGetErrorString(e));
