@@ -46,9 +46,18 @@
 // TMEM columns: [0,144) [144,288) accumulators, then NA A-operand buffers.
 #include <stdlib.h>
 #include <cuda_fp8.h>
+#include <type_traits>
 
 #include "dyq_internal.cuh"
 #include "dyq_ptx.cuh"
+
+// timing-only build switches (tools/build_variant.py), 0 in product builds
+#ifndef DYQ_EXP_MASK
+#define DYQ_EXP_MASK 0
+#endif
+#ifndef DYQ_PREFILL_TRACE
+#define DYQ_PREFILL_TRACE 0
+#endif
 
 namespace dyq {
 
@@ -113,6 +122,9 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
     uint8_t* s_col = smem + 512;  // per token column: 0 absent, 1 integer bits, 2 BF16 bypass
     // per-group event ev of CTA (0,0): a plain store at trace[16 + 512 ev + g]
     // (no atomics: tracing adds no latency to the pipeline it observes)
+    // (compiled in only with -DDYQ_PREFILL_TRACE=1, tools/build_variant.py:
+    // even untaken, the checks cost the hot loops ~5 %)
+#if DYQ_PREFILL_TRACE
     uint64_t* const tr = (blockIdx.x == 0 && blockIdx.y == 0) ? a.trace : nullptr;
     auto tev = [&](uint32_t ev, int g) {
         if (tr && g < 512) {
@@ -121,6 +133,9 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             tr[16 + 512 * ev + g] = t;
         }
     };
+#else
+    auto tev = [](uint32_t, int) {};
+#endif
     uint8_t* stage0 = smem + 1024;
 
     ptx::pdl_wait();  // the B operand, s_x and row_bits come from the preceding kernels
@@ -133,7 +148,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
         ok8 &= (bm == 2 || bm == 4);
     }
     // tile mode (uniform per CTA; the quantizer decides identically)
-    const bool f8 = __syncthreads_and(ok8) && WBITS == 4 && a.e4m3;
+    const bool f8 = WBITS == 4 && a.e4m3 && __syncthreads_and(ok8);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -170,9 +185,6 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 if (g >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
                 // (DYQ_EXP_NO_* : timing experiments only, tools/build_variant.py)
-#ifndef DYQ_EXP_MASK
-#define DYQ_EXP_MASK 0
-#endif
                 constexpr int XM = DYQ_EXP_MASK;  // bit 0 codes, 1 meta, 2 B, 3 s_x skipped
                 ptx::mbar_arrive_expect_tx(&full[s], (XM & 1 ? 0 : cbytes) + (XM & 2 ? 0 : META_BLOCK) +
                                                          (XM & 4 ? 0 : bbytes) + (XM & 8 ? 0 : PAR_BYTES));
@@ -235,6 +247,9 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
         // step -- exactly the 16x256b register fragment, so each sub-tile and
         // slab pair is one LDS.128 and one tcgen05.st.16x256b.x4.
         const int q = warp & 3;
+        // one loop per tile mode (the mode is uniform per CTA): no per-group branch
+        auto transform = [&](auto f8c) {
+        constexpr bool F8 = decltype(f8c)::value;
         int s = 0, ai = 0;
         uint32_t ph = 0, aph = 0;
         for (int g = 0; g < NG; ++g) {
@@ -251,7 +266,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 const uint32_t tl = at + ((uint32_t)(32 * q + 16 * si) << 16);
                 // zero points of rows gid and gid+8 are adjacent metadata slots
                 const uint32_t z01 = *reinterpret_cast<const uint16_t*>(zrow + sub * 16 + 2 * (lane >> 2));
-                if (WBITS == 4 && f8) {
+                if constexpr (WBITS == 4 && F8) {
                     // e4m3 (q - z_w): K step = slab; TMEM column 2t <- low nibbles,
                     // 2t + 1 <- high nibbles (e4m3_kpos), rows gid / gid + 8
                     const float zf0 = 8388608.f + (float)(z01 & 0xffu), zf1 = 8388608.f + (float)(z01 >> 8);
@@ -348,6 +363,11 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             if (++s == S) { s = 0; ph ^= 1; }
             if (++ai == NA) { ai = 0; aph ^= 1; }
         }
+        };
+        if (f8)
+            transform(std::true_type{});
+        else
+            transform(std::false_type{});
     } else {
         // ------------------------------------------------------ promotion
         // 16x256b loads: thread (gid, t) holds rows 32q + 16 si + gid (+8) and
@@ -501,13 +521,14 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
     const int m = tt * PT + row;
     const int b = m < M ? (row_bits ? row_bits[m] : bits) : 0;
     // tile mode (dyq_pre_tile_e4m3): every present token of tile tt at A2 / A4
-    int ok8 = 1;
-    for (int i = lane; i < PT; i += 32) {
-        const int mm = tt * PT + i;
-        const int bm = mm < M ? (row_bits ? row_bits[mm] : bits) : 2;
-        ok8 &= (bm == 2 || bm == 4);
-    }
-    const bool f8 = __all_sync(0xffffffffu, ok8) && e4m3_ok;
+    int ok8 = e4m3_ok;
+    if (e4m3_ok)
+        for (int i = lane; i < PT; i += 32) {
+            const int mm = tt * PT + i;
+            const int bm = mm < M ? (row_bits ? row_bits[mm] : bits) : 2;
+            ok8 &= (bm == 2 || bm == 4);
+        }
+    const bool f8 = __all_sync(0xffffffffu, ok8) != 0;
     uint8_t* xg = act + P.x16_off + tg * P.x16_group;
     auto x8_at = [&](int k) -> uint8_t* {  // e4m3 B operand: 32 k per K step, 32 B per row
         const int ks = k >> 5, p = e4m3_kpos(k & 31);

@@ -1,6 +1,8 @@
 """Per-group pipeline timeline of the prefill kernel, CTA (0,0), from the
 non-blocking trace (dyq_trace_enable; buffer slots 16 + 512 ev + g).
-usage: python tools/trace_prefill.py [linear] [M] [bits]   (DYQ_PRE_E4M3=1 for e4m3)"""
+usage: python tools/build_variant.py trace -DDYQ_PREFILL_TRACE=1
+       DYQ_LIB=tools/variants/libdyq_trace.so python tools/trace_prefill.py [linear] [M] [bits]
+(the product build compiles the per-group hooks out; DYQ_PRE_E4M3=1 for the e4m3 path)"""
 import os
 import sys
 
