@@ -51,7 +51,7 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
         }
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+    bad = warp_min_i(bad);
     if (bad != 0x7fffffff && lane == 0)
         report_nonfinite(err, (int64_t)(m0 + m) * L.K + (int64_t)g * L.G + bad);
     if (b != 2 && b != 4 && b != 8) {  // padding row or BF16 bypass row

@@ -195,21 +195,18 @@ __device__ __forceinline__ uint16_t silu_mul_bf16(uint16_t gb, uint16_t ub) {
 }
 
 // -------------------------------------------------------------- warp ops
-__device__ inline float warp_min(float v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
+// Warp reductions with one REDUX instruction each (sm_80+).  Floats go through
+// an order-preserving int map (exact: min / max return an input value; the
+// callers' values are finite or already reported as non-finite).
+__device__ __forceinline__ int f2ord(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
 }
-__device__ inline float warp_max(float v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-__device__ inline int warp_sum_i(int v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+__device__ inline float warp_min(float v) { return ord2f(__reduce_min_sync(0xffffffffu, f2ord(v))); }
+__device__ inline float warp_max(float v) { return ord2f(__reduce_max_sync(0xffffffffu, f2ord(v))); }
+__device__ inline int warp_sum_i(int v) { return __reduce_add_sync(0xffffffffu, v); }
+__device__ inline int warp_min_i(int v) { return __reduce_min_sync(0xffffffffu, v); }
 
 size_t decode_ws_bytes(const WLayout& L);
 dyq_status_t launch_prefetch_l2(const void* p, size_t bytes, cudaStream_t st);
