@@ -332,6 +332,62 @@ DYQ_API dyq_status_t dyq_tp_allgather(void* comm, const uint16_t* y_shard, int32
 DYQ_API dyq_status_t dyq_tp_interleave(const uint16_t* buf, int32_t P, int32_t M, int32_t Ns, uint16_t* y,
                                        dyq_stream_t stream);
 
+/* ------------------------------------------- offline threshold calibration */
+/* PAPER.md §IV-B: eps_a(S) = D_acc / (S + eta); Eq. (5)
+ * minimal bits under the bound; Theta = {theta_24, theta_48} from
+ * calibration trajectories, in SPEC's binned isotonic reading
+ * with DESIGN.md readings C1-C6.
+ *
+ * Forced-bits policy step: like dyq_policy_step, but episode e runs at the
+ * given b*_t = bits[e] (device int32 [E], values in {2,4,8,16}) and no
+ * selection state is read or updated. */
+DYQ_API dyq_status_t dyq_policy_step_bits(void* model, int32_t E, const int32_t* bits, const uint16_t* vis_emb,
+                                          const int32_t* text_ids, float* action_out, dyq_stream_t stream);
+/* One calibration step for Ec control streams ("executing the
+ * full-precision model on a representative calibration subset"):
+ *   1. S_t of every stream from a*_{t-1} (dyq_select_bits on `state`, >= Ec
+ *      streams; NULL action at the model's first step) -> S_out (device f64 [Ec]);
+ *   2. ONE batched policy step over 4 Ec replicas of the observations
+ *      (vis_emb [Ec, n_vis, d], text_ids [Ec, n_text]) at b = 16 | 2 | 4 | 8:
+ *      actions_out (device f32 [4 Ec, n_act]) rows [0, Ec) = a*_t (BF16 path,
+ *      which the next step's S observes), rows [(j+1) Ec, (j+2) Ec) = a^(b_j);
+ *   3. err_out (device f64 [Ec, 3]) = || a^(b) - a* ||_2, b = 2, 4, 8.
+ * Requires 4 Ec <= desc.E.  The counterfactual actions never drive the
+ * trajectory (the environment steps with a*). */
+DYQ_API dyq_status_t dyq_calib_collect(void* model, void* state, int32_t Ec, const uint16_t* vis_emb,
+                                       const int32_t* text_ids, float* actions_out, double* S_out,
+                                       double* err_out, dyq_stream_t stream);
+/* err_out[e, j] = || a[(j+1) Ec + e, :] - a[e, :] ||_2 (fp64, j = 0..2), a
+ * device f32 [4 Ec, n_act]: step 3 of dyq_calib_collect on its own. */
+DYQ_API dyq_status_t dyq_calib_errors(const float* actions, int32_t Ec, int32_t n_act, double* err_out,
+                                      dyq_stream_t stream);
+/* Derive Theta (HOST pointers; offline).  S host f64 [n], err host f64 [n, 3]
+ * = (e^(2), e^(4), e^(8)) per step.  calib: reads theta_fp, D_acc, eta (> 0),
+ * writes theta_24 <= theta_48 <= theta_fp; other fields untouched.
+ *   - samples with S outside [0, theta_fp] are ignored (BF16 steps);
+ *   - n_bins uniform bins on [0, theta_fp] (SPEC: 32); mean e^(2), e^(4) per
+ *     bin; bins with >= n_min samples (SPEC: 50) get a count-weighted
+ *     isotonic (non-decreasing) fit, the others are interpolated between
+ *     covered neighbours (coverage warning: *n_undercovered);
+ *   - theta_24 = lower edge of the first bin whose smoothed e^(2) exceeds
+ *     eps_a at the bin's upper edge, else theta_fp; theta_48 likewise with
+ *     e^(4), raised to theta_24 if below.
+ * Optional outputs (NULL to skip): smoothed [2, n_bins], counts [n_bins].
+ * Errors: DYQ_EINVAL for n <= 0, bad parameters, or no bin with n_min samples.
+ * Deterministic: sequential fp64 sums in sample order. */
+DYQ_API dyq_status_t dyq_calib_derive(const double* S, const double* err, int64_t n, int32_t n_bins,
+                                      int32_t n_min, dyq_calib_t* calib, double* smoothed,
+                                      int64_t* counts, int32_t* n_undercovered);
+/* Audit a table on (held-out) samples (HOST pointers): a sample
+ * with S in [0, theta_fp] runs b = Phi(S) (Eq. (6)) and is satisfied iff
+ * e^(b) <= eps_a(S); others run BF16 and are satisfied.  n_quant = samples in
+ * the quantized domain, n_ok = satisfied samples (of n), worst [n_bins]
+ * (or NULL) = per-bin max e^(b) / eps_a(S), 0 for empty bins.  n = 0 is
+ * valid (zero counts).  DYQ_EINVAL if the thresholds are not ordered. */
+DYQ_API dyq_status_t dyq_calib_validate(const dyq_calib_t* calib, const double* S, const double* err,
+                                        int64_t n, int32_t n_bins, int64_t* n_quant, int64_t* n_ok,
+                                        double* worst);
+
 #ifdef __cplusplus
 }
 #endif

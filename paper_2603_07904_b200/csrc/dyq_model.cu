@@ -642,12 +642,12 @@ __global__ void head_argmax_kernel(const uint16_t* __restrict__ x, int row_strid
 // h rows of the prefill sequence: vision embeddings, then text-token embeddings
 __global__ void embed_prefill_kernel(const uint16_t* __restrict__ vis, const int32_t* __restrict__ text,
                                      const uint16_t* __restrict__ embed, int n_vis, int n_text, int d,
-                                     uint16_t* __restrict__ h) {
+                                     uint16_t* __restrict__ h, int src_E) {
     ptx::pdl_wait();
     ptx::pdl_launch_dependents();
     const int S = n_vis + n_text;
     const int row = blockIdx.x;  // e * S + i
-    const int e = row / S, i = row % S;
+    const int e = (row / S) % src_E, i = row % S;  // replicas e, e + src_E, ... share an observation
     const uint16_t* src = i < n_vis ? vis + ((size_t)e * n_vis + i) * d
                                     : embed + (size_t)text[(size_t)e * n_text + (i - n_vis)] * d;
     for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8)
@@ -996,10 +996,14 @@ dyq_status_t dyq_model_free(void* model) {
     return DYQ_OK;
 }
 
-dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t* vis, const int32_t* text,
-                             float* action_out, int32_t* bits_out, dyq_stream_t stream) {
+// One control step.  forced == nullptr: b*_t from the selection state (the
+// product path); else per-episode bits forced[E] (device) and no selection.
+// Episode e reads observation e % src_E (calibration replicas).
+static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* forced, int32_t src_E, int32_t E,
+                                     const uint16_t* vis, const int32_t* text, float* action_out, int32_t* bits_out,
+                                     dyq_stream_t stream) {
     Model* m = reinterpret_cast<Model*>(model);
-    if (!m || !state || !vis || !text || !action_out) return set_error(DYQ_EINVAL, "null pointer");
+    if (!m || (!state && !forced) || !vis || !text || !action_out) return set_error(DYQ_EINVAL, "null pointer");
     const dyq_model_desc_t& D = m->d;
     const ModelLayout& L = m->L;
     if (E <= 0 || E > D.E) return set_error(DYQ_EINVAL, "E = %d outside [1, %d]", E, D.E);
@@ -1033,8 +1037,15 @@ dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t
     for (int i = 0; i < 4; ++i) wd[i] = wdesc_of(D, i);
 
     // b*_t from a_{t-1}, then per-row activation bits (W4-pinned table)
-    DYQ_TRY(dyq_select_route(state, E, m->t == 0 ? nullptr : prev, bits, S, nullptr, rbp, nullptr, nullptr, stream));
-    DYQ_TRY(dyq_route_bits(bits, E, 1, nullptr, rbd, stream));
+    if (forced) {
+        DYQ_TRY(dyq_route_bits(forced, E, S, nullptr, rbp, stream));
+        DYQ_TRY(dyq_route_bits(forced, E, 1, nullptr, rbd, stream));
+        bits = const_cast<int32_t*>(forced);  // detok copies it to bits_out
+    } else {
+        DYQ_TRY(dyq_select_route(state, E, m->t == 0 ? nullptr : prev, bits, S, nullptr, rbp, nullptr, nullptr,
+                                 stream));
+        DYQ_TRY(dyq_route_bits(bits, E, 1, nullptr, rbd, stream));
+    }
 
     auto layer = [&](int l, int M, int32_t* rb, bool prefill, int pos) -> dyq_status_t {
         const size_t li = (size_t)4 * l;
@@ -1060,7 +1071,8 @@ dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t
     };
 
     // ---- prefill: vision + text tokens
-    if (launch_pdl(embed_prefill_kernel, dim3(MP), dim3(128), 0, st, vis, text, D.embed, D.n_vis, D.n_text, d, h) !=
+    if (launch_pdl(embed_prefill_kernel, dim3(MP), dim3(128), 0, st, vis, text, D.embed, D.n_vis, D.n_text, d, h,
+                   src_E) !=
         cudaSuccess)
         return set_error(DYQ_ECUDA, "embed_prefill_kernel launch");
     DYQ_TRY(check_launch("embed_prefill_kernel"));
@@ -1084,6 +1096,67 @@ dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t
 #undef DYQ_TRY
     m->t += 1;
     return DYQ_OK;
+}
+
+dyq_status_t dyq_policy_step(void* model, void* state, int32_t E, const uint16_t* vis, const int32_t* text,
+                             float* action_out, int32_t* bits_out, dyq_stream_t stream) {
+    if (!state) return set_error(DYQ_EINVAL, "null state");
+    return policy_step_impl(model, state, nullptr, E, E, vis, text, action_out, bits_out, stream);
+}
+
+dyq_status_t dyq_policy_step_bits(void* model, int32_t E, const int32_t* bits, const uint16_t* vis,
+                                  const int32_t* text, float* action_out, dyq_stream_t stream) {
+    if (!bits) return set_error(DYQ_EINVAL, "null bits");
+    return policy_step_impl(model, nullptr, bits, E, E, vis, text, action_out, nullptr, stream);
+}
+
+// e[e, j] = || a[(j+1) Ec + e, :] - a[e, :] ||_2 in fp64, j = 0..2 (b = 2, 4, 8)
+__global__ void calib_errors_kernel(const float* __restrict__ a, int Ec, int n_act, double* __restrict__ e_out) {
+    ptx::pdl_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * Ec) return;
+    const int e = i / 3, j = i % 3;
+    const float* ref = a + (size_t)e * n_act;
+    const float* q = a + ((size_t)(j + 1) * Ec + e) * n_act;
+    double acc = 0.0;
+    for (int k = 0; k < n_act; ++k) {
+        const double d = (double)q[k] - (double)ref[k];
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    e_out[i] = __dsqrt_rn(acc);
+}
+
+__global__ void calib_bits_kernel(int Ec, int32_t* __restrict__ bits) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 4 * Ec) bits[i] = (i < Ec) ? 16 : (2 << (i / Ec - 1));  // 16 | 2 | 4 | 8
+}
+
+dyq_status_t dyq_calib_errors(const float* actions, int32_t Ec, int32_t n_act, double* err_out, dyq_stream_t stream) {
+    if (!actions || !err_out) return set_error(DYQ_EINVAL, "null pointer");
+    if (Ec <= 0 || n_act <= 0) return set_error(DYQ_ESHAPE, "Ec = %d, n_act = %d", Ec, n_act);
+    if (launch_pdl(calib_errors_kernel, dim3((3 * Ec + 127) / 128), dim3(128), 0, (cudaStream_t)stream, actions, Ec,
+                   n_act, err_out) != cudaSuccess)
+        return set_error(DYQ_ECUDA, "calib_errors_kernel launch");
+    return check_launch("calib_errors_kernel");
+}
+
+dyq_status_t dyq_calib_collect(void* model, void* state, int32_t Ec, const uint16_t* vis, const int32_t* text,
+                               float* actions_out, double* S_out, double* err_out, dyq_stream_t stream) {
+    Model* m = reinterpret_cast<Model*>(model);
+    if (!m || !state || !vis || !text || !actions_out || !S_out || !err_out)
+        return set_error(DYQ_EINVAL, "null pointer");
+    if (Ec <= 0 || 4 * Ec > m->d.E) return set_error(DYQ_EINVAL, "4 * Ec = %d outside [4, E = %d]", 4 * Ec, m->d.E);
+    const ModelLayout& L = m->L;
+    int32_t* bits = m->at<int32_t>(L.bits);
+    float* prev = m->at<float>(L.prev);       // a*_{t-1} of stream e at prev[e * 7] (FP replicas first)
+    const cudaStream_t st = (cudaStream_t)stream;
+    dyq_status_t rc = dyq_select_bits(state, Ec, m->t == 0 ? nullptr : prev, bits, S_out, nullptr, stream);
+    if (rc) return rc;
+    int32_t* fb = bits;  // [desc.E >= 4 Ec]: b*_t of the selection above is not used
+    calib_bits_kernel<<<(4 * Ec + 127) / 128, 128, 0, st>>>(Ec, fb);
+    if ((rc = check_launch("calib_bits_kernel"))) return rc;
+    if ((rc = policy_step_impl(model, nullptr, fb, Ec, 4 * Ec, vis, text, actions_out, nullptr, stream))) return rc;
+    return dyq_calib_errors(actions_out, Ec, m->d.n_act, err_out, stream);
 }
 
 }  // extern "C"

@@ -59,6 +59,11 @@ _SIGS = {
     "dyq_comm_destroy": [P],
     "dyq_tp_allgather": [P, P, i32, i32, P, P, P],
     "dyq_tp_interleave": [P, i32, i32, i32, P, P],
+    "dyq_policy_step_bits": [P, i32, P, P, P, P, P],
+    "dyq_calib_collect": [P, P, i32, P, P, P, P, P, P],
+    "dyq_calib_errors": [P, i32, i32, P, P],
+    "dyq_calib_derive": [P, P, i64, i32, i32, P, P, P, P],
+    "dyq_calib_validate": [P, P, P, i64, i32, P, P, P],
 }
 _RESTYPES = {"dyq_last_error": C.c_char_p, "dyq_version": C.c_char_p}
 
@@ -393,6 +398,17 @@ class Model:
         _call("dyq_policy_step", self._h, _ptr(state), E, _ptr(vis_emb), _ptr(text_ids), _ptr(action_out),
               _ptr(bits_out), _stream(stream))
 
+    def step_bits(self, E: int, bits, vis_emb, text_ids, action_out, stream=None):
+        """Forced-bits step: episode e runs at bits[e] (device int32 [E])."""
+        _call("dyq_policy_step_bits", self._h, E, _ptr(bits), _ptr(vis_emb), _ptr(text_ids), _ptr(action_out),
+              _stream(stream))
+
+    def calib_collect(self, state, Ec: int, vis_emb, text_ids, actions_out, S_out, err_out, stream=None):
+        """One calibration step (dyq_calib_collect): S_t, a* and the
+        counterfactual 2/4/8-bit actions in one batched step, e^(b)."""
+        _call("dyq_calib_collect", self._h, _ptr(state), Ec, _ptr(vis_emb), _ptr(text_ids), _ptr(actions_out),
+              _ptr(S_out), _ptr(err_out), _stream(stream))
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
@@ -401,6 +417,47 @@ class Model:
             except Exception:
                 pass
             self._h = None
+
+
+# ------------------------------------------- offline threshold calibration
+def calib_errors(actions, Ec: int, n_act: int, err_out, stream=None):
+    _call("dyq_calib_errors", _ptr(actions), Ec, n_act, _ptr(err_out), _stream(stream))
+
+
+def _host_f64(a, cols=None):
+    import numpy as np
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if cols is not None:
+        a = a.reshape(-1, cols)
+    return a, a.ctypes.data_as(C.c_void_p)
+
+
+def calib_derive(S, err, calib: Calib, n_bins: int = 32, n_min: int = 50):
+    """Host arrays S [n], err [n, 3]; fills calib.theta_24 / theta_48 and
+    returns (smoothed [2, n_bins], counts [n_bins], n_undercovered)."""
+    import numpy as np
+    S, pS = _host_f64(S)
+    err, pE = _host_f64(err, 3)
+    if err.shape[0] != S.size:
+        raise ValueError("S and err disagree on the sample count")
+    sm = np.zeros((2, n_bins), np.float64)
+    cnt = np.zeros(n_bins, np.int64)
+    und = C.c_int32(0)
+    _call("dyq_calib_derive", pS, pE, S.size, n_bins, n_min, C.byref(calib), sm.ctypes.data_as(C.c_void_p),
+          cnt.ctypes.data_as(C.c_void_p), C.byref(und))
+    return sm, cnt, und.value
+
+
+def calib_validate(calib: Calib, S, err, n_bins: int = 32):
+    """Returns (n_quant, n_ok, worst [n_bins]) for host arrays S [n], err [n, 3]."""
+    import numpy as np
+    S, pS = _host_f64(S)
+    err, pE = _host_f64(err, 3)
+    worst = np.zeros(n_bins, np.float64)
+    nq, nok = C.c_int64(0), C.c_int64(0)
+    _call("dyq_calib_validate", C.byref(calib), pS, pE, S.size, n_bins, C.byref(nq), C.byref(nok),
+          worst.ctypes.data_as(C.c_void_p))
+    return nq.value, nok.value, worst
 
 
 # ------------------------------------------------------ tensor parallelism
