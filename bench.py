@@ -544,6 +544,37 @@ def main():
                             "policy_steps_per_s": round(sps, 2)}
             del gp, model
             torch.cuda.empty_cache()
+        # offline calibration collection (NEXT-3): Ec streams, one batched step of
+        # 4 Ec replicas at b = 16 | 2 | 4 | 8 per calibration step
+        Ec = 2
+        model = dyq.Model(layers, norms, norms, one, embed, head, E=4 * Ec, n_heads=32)
+        cal = dyq.default_calib()
+        pst = torch.zeros(dyq.state_size(Ec, cal), dtype=torch.uint8, device=dev)
+        dyq.state_init(Ec, cal, pst)
+        vis = synth.activations_bf16_torch(Ec * 256, d_m, seed=7300 + rank, device=dev)
+        gen = torch.Generator(device=dev).manual_seed(7400 + rank)
+        text = torch.randint(0, 32000, (Ec, 32), dtype=torch.int32, device=dev, generator=gen)
+        acts_c = torch.zeros(4 * Ec, 7, dtype=torch.float32, device=dev)
+        S_c = torch.zeros(Ec, dtype=torch.float64, device=dev)
+        e_c = torch.zeros(Ec, 3, dtype=torch.float64, device=dev)
+        for _ in range(2):
+            model.calib_collect(pst, Ec, vis, text, acts_c, S_c, e_c)
+        torch.cuda.synchronize()
+        R = 3
+        gp = torch.cuda.CUDAGraph()
+        sp = torch.cuda.Stream()
+        sp.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(gp, stream=sp):
+            for _ in range(R):
+                model.calib_collect(pst, Ec, vis, text, acts_c, S_c, e_c, stream=sp)
+        gp.replay()
+        torch.cuda.synchronize()
+        ms = statistics.median(timed(gp) for _ in range(3)) / R
+        pres[f"calib_Ec{Ec}"] = {"streams_per_gpu": Ec, "replicas": 4 * Ec, "ms_per_step": round(ms, 3),
+                                 "calib_steps_per_s": round(episodes.throughput(Ec, ms * 1e-3), 2),
+                                 "what": "dyq_calib_collect: S_t + a* + a^(2,4,8) + e^(b) per stream-step"}
+        del gp, model
+        torch.cuda.empty_cache()
         policy = {"workload": "configs[3] slice: dyq_policy_step, OpenVLA-7B shapes (32 blocks, d=4096, "
                               "ffn=11008, 32 heads), 256 vision + 32 text tokens, 7 action tokens, W4 G64, "
                               "per-episode b* from the kinematic dispatcher",

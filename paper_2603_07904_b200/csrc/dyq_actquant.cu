@@ -50,7 +50,6 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
             vmax = fmaxf(vmax, v[i]);
         }
     }
-#pragma unroll
     bad = warp_min_i(bad);
     if (bad != 0x7fffffff && lane == 0)
         report_nonfinite(err, (int64_t)(m0 + m) * L.K + (int64_t)g * L.G + bad);
