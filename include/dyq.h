@@ -332,6 +332,44 @@ DYQ_API dyq_status_t dyq_tp_allgather(void* comm, const uint16_t* y_shard, int32
 DYQ_API dyq_status_t dyq_tp_interleave(const uint16_t* buf, int32_t P, int32_t M, int32_t Ns, uint16_t* y,
                                        dyq_stream_t stream);
 
+/* -------------------------- fused tensor-parallel decode epilogue (NEXT-1) */
+/* The all-gather of the column shards folded into the decode kernel: rank r's
+ * epilogue stores y[:, r Ns + j] (bf16) straight into EVERY rank's full output
+ * y[p] ([M, world * Ns], peer memory over NVLink / NVSwitch, mapped with
+ * dyq_ipc_open); each CTA then fences at system scope and adds the number of
+ * 16-column sub-tiles it wrote to every rank's flag[p] (Ns / 16 per call in
+ * total).  After the c-th call on every rank, each flag
+ * reaches c * world * Ns / 16 = c * N / 16; dyq_tp_wait orders a rank's stream
+ * after that point.  Consecutive calls must alternate between two y buffers
+ * (a peer may start call c+1 while this rank still reads call c's output).
+ * Decode only (M <= 16; DYQ_EUNSUPPORTED above: use dyq_tp_allgather).
+ * wd = this rank's shard descriptor (N = Ns, dyq_tp_shard rows). */
+#define DYQ_TP_MAX 8
+typedef struct {
+    int32_t world, rank;
+    void* y[DYQ_TP_MAX];        /* rank p's full y as mapped in this process   */
+    uint64_t* flag[DYQ_TP_MAX]; /* rank p's arrival counter (u64, zeroed once) */
+} dyq_tp_peers_t;
+DYQ_API dyq_status_t dyq_qlinear_tp(const dyq_wdesc_t* wd, const void* codes, const void* meta,
+                                    const uint16_t* x, int32_t M, const int32_t* row_bits, int32_t bits,
+                                    const dyq_tp_peers_t* peers, void* workspace, size_t ws_bytes,
+                                    int64_t* err, dyq_stream_t stream);
+/* Stream-ordered wait until *flag >= target (device u64, ld.acquire.sys).
+ * Bounded: after 10 s the kernel sets *timed_out = 1 (device int32, may be
+ * NULL) and returns rather than hang the GPU. */
+DYQ_API dyq_status_t dyq_tp_wait(const uint64_t* flag, uint64_t target, int32_t* timed_out,
+                                 dyq_stream_t stream);
+/* CUDA IPC of device buffers, for peer y / flag buffers of other processes.
+ * A handle (64 B) names the whole allocation holding dev_ptr (e.g. a caching
+ * allocator segment); offset_out = dev_ptr - allocation base.  The caller
+ * exchanges (handle, offset) (e.g. over the torch process group); dyq_ipc_open
+ * returns the peer's dev_ptr in this process.  One open per peer allocation
+ * (CUDA refuses to map the same allocation twice): keep a rank's y buffers and
+ * flag in one allocation.  dyq_ipc_close(ptr, offset) unmaps. */
+DYQ_API dyq_status_t dyq_ipc_handle(void* dev_ptr, void* handle_out, uint64_t* offset_out);
+DYQ_API dyq_status_t dyq_ipc_open(const void* handle, uint64_t offset, void** dev_ptr);
+DYQ_API dyq_status_t dyq_ipc_close(void* dev_ptr, uint64_t offset);
+
 /* ------------------------------------------- offline threshold calibration */
 /* PAPER.md §IV-B: eps_a(S) = D_acc / (S + eta); Eq. (5)
  * minimal bits under the bound; Theta = {theta_24, theta_48} from

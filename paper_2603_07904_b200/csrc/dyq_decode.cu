@@ -61,6 +61,7 @@ struct DecArgs {
     int off_meta, off_cp, off_x16;  // offsets inside a stage
     uint64_t* trace;                // dyq_trace_enable buffer or null
     uint32_t serial;
+    TpPeers tp;                     // fused TP epilogue (tp.n = 0: off)
 };
 
 __device__ __forceinline__ void mma_u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -165,7 +166,9 @@ __device__ __forceinline__ void dec_publish(int*& pend, int lane) {
 // acquires the counter, adds the slots in contributor order (deterministic)
 // to its own partial sums and writes y.  All CTAs of the grid are co-resident
 // (grid <= #SMs, one CTA per SM), so the reducer's wait always ends.
-template <int NT8>
+__shared__ int s_tp_subtiles;  // fused TP: sub-tiles of y this CTA wrote
+
+template <int NT8, bool TP>
 __device__ __forceinline__ void dec_flush_warp(const DecArgs& a, int tile, const float (&facc)[NT8][4], int sub,
                                                int lane, int*& pend) {
     const WLayout& L = a.L;
@@ -178,6 +181,12 @@ __device__ __forceinline__ void dec_flush_warp(const DecArgs& a, int tile, const
     const int nc = c_last - c_first + 1;
     const int c = (int)blockIdx.x - c_first;
     auto store = [&](int tok, int r, float v) {
+        if constexpr (TP) {  // every rank's full y, this rank's columns
+            const size_t o = (size_t)(a.m0 + tok) * a.tp.ldy + a.tp.col0 + tile * 128 + sub * 16 + r;
+            const __nv_bfloat16 h = __float2bfloat16_rn(v);
+            for (int p = 0; p < a.tp.n; ++p) reinterpret_cast<__nv_bfloat16*>(a.tp.y[p])[o] = h;
+            return;
+        }
         const size_t o = (size_t)(a.m0 + tok) * L.N + tile * 128 + sub * 16 + r;
         if (a.y_dtype == 0)
             reinterpret_cast<float*>(a.y)[o] = v;
@@ -252,6 +261,25 @@ __device__ __forceinline__ void dec_flush_warp(const DecArgs& a, int tile, const
             const int tok = j * 8 + 2 * t + (i & 1);
             if (tok < a.M) store(tok, gid + 8 * (i >> 1), v[j][i]);
         }
+    if constexpr (TP) {  // counted here, announced once per CTA (dec_tp_announce)
+        __syncwarp();
+        if (lane == 0) atomicAdd_block(&s_tp_subtiles, 1);
+    }
+}
+
+// Fused TP: after every consumer warp is done, one thread fences at system
+// scope (the CTA barrier orders all warps' peer stores before it) and adds
+// the CTA's sub-tile count to every rank's flag -- one fence and tp.n atomics
+// per CTA instead of per 16-column sub-tile.
+__device__ __forceinline__ void dec_tp_announce(const DecArgs& a) {
+    ptx::named_bar_sync(9, DEC_CWARPS * 32);
+    if (threadIdx.x == 0) {
+        const int n = s_tp_subtiles;
+        if (n) {
+            __threadfence_system();  // fence.acq_rel.sys / red.release.sys / gpu scope: no faster
+            for (int p = 0; p < a.tp.n; ++p) atomicAdd_system(a.tp.flag[p], (unsigned long long)n);
+        }
+    }
 }
 
 // One group (unit) of one 16-row sub-tile for this warp.  `st` = stage base
@@ -411,7 +439,7 @@ __device__ __forceinline__ void dec_group(const DecArgs& a, uint32_t st, int gi,
 // End of this CTA's part of a tile: with 16 consumer warps the odd-group warp
 // of each sub-tile hands its partial sums to the even-group warp (shared
 // memory + a 64-thread named barrier per sub-tile), which flushes.
-template <int NT8>
+template <int NT8, bool TP>
 __device__ __forceinline__ void dec_tile_done(const DecArgs& a, int tile, float (&facc)[NT8][4], int sub, int par,
                                               int lane, int*& pend) {
     if constexpr (DEC_CWARPS == 16) {
@@ -433,12 +461,12 @@ __device__ __forceinline__ void dec_tile_done(const DecArgs& a, int tile, float 
         ptx::named_bar_sync(1 + sub, 64);
         if (par == 1) return;
     }
-    dec_flush_warp<NT8>(a, tile, facc, sub, lane, pend);
+    dec_flush_warp<NT8, TP>(a, tile, facc, sub, lane, pend);
 }
 
 // Consumer loop over the CTA's stages (must enumerate stages exactly like the
 // producer).  Consumer warp w works on sub-tile w for every group.
-template <int WBITS, int NT8, int SPG, int MODE, bool PARTIALS>
+template <int WBITS, int NT8, int SPG, int MODE, bool PARTIALS, bool TP>
 __device__ __forceinline__ void dec_consume(const DecArgs& a, uint32_t bar_full, uint32_t bar_empty,
                                             uint32_t stage0, int u0, int u1, uint32_t is16_mask) {
     const WLayout& L = a.L;
@@ -464,7 +492,7 @@ __device__ __forceinline__ void dec_consume(const DecArgs& a, uint32_t bar_full,
         n = n < gps ? n : gps;
         n = n < u1 - u ? n : u1 - u;
         if (!PARTIALS && tile != cur_tile) {
-            if (cur_tile >= 0) dec_tile_done<NT8>(a, cur_tile, facc, sub, par, lane, pend);
+            if (cur_tile >= 0) dec_tile_done<NT8, TP>(a, cur_tile, facc, sub, par, lane, pend);
             cur_tile = tile;
 #pragma unroll
             for (int j = 0; j < NT8; ++j)
@@ -488,13 +516,13 @@ __device__ __forceinline__ void dec_consume(const DecArgs& a, uint32_t bar_full,
         g0 += n;
     }
     if constexpr (!PARTIALS) {
-        if (cur_tile >= 0) dec_tile_done<NT8>(a, cur_tile, facc, sub, par, lane, pend);
+        if (cur_tile >= 0) dec_tile_done<NT8, TP>(a, cur_tile, facc, sub, par, lane, pend);
         dec_publish(pend, lane);
     }
     if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 1, 4);
 }
 
-template <int WBITS, int NT8, int SPG, bool PARTIALS>
+template <int WBITS, int NT8, int SPG, bool PARTIALS, bool TP>
 __global__ void __launch_bounds__(DEC_THREADS, NT8 == 1 ? DEC_MINB : 1) qlinear_decode_kernel(const DecArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const WLayout& L = a.L;
@@ -517,6 +545,7 @@ __global__ void __launch_bounds__(DEC_THREADS, NT8 == 1 ? DEC_MINB : 1) qlinear_
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], DEC_CWARPS);
         }
+        if constexpr (TP) s_tp_subtiles = 0;
         ptx::fence_mbar_init();
         trace_ev(a.trace, a.serial, 1, 0);
     }
@@ -612,13 +641,14 @@ __global__ void __launch_bounds__(DEC_THREADS, NT8 == 1 ? DEC_MINB : 1) qlinear_
     const uint32_t bar_full = ptx::smem_u32(full), bar_empty = ptx::smem_u32(empty);
     const uint32_t st0 = ptx::smem_u32(stage0);
     if (!any16 && dec_call_centred(a.M, a.m0, a.row_bits, a.bits))
-        dec_consume<WBITS, NT8, SPG, MODE_INTC, PARTIALS>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
+        dec_consume<WBITS, NT8, SPG, MODE_INTC, PARTIALS, TP>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
     else if (PARTIALS || (any_int && any16))
-        dec_consume<WBITS, NT8, SPG, MODE_MIXED, PARTIALS>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
+        dec_consume<WBITS, NT8, SPG, MODE_MIXED, PARTIALS, TP>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
     else if (any16)
-        dec_consume<WBITS, NT8, SPG, MODE_A16, PARTIALS>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
+        dec_consume<WBITS, NT8, SPG, MODE_A16, PARTIALS, TP>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
     else
-        dec_consume<WBITS, NT8, SPG, MODE_INT, PARTIALS>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
+        dec_consume<WBITS, NT8, SPG, MODE_INT, PARTIALS, TP>(a, bar_full, bar_empty, st0, u0, u1, is16_mask);
+    if constexpr (TP) dec_tp_announce(a);
 }
 
 // ------------------------------------------------------------------ host
@@ -685,12 +715,12 @@ size_t decode_ws_bytes(const WLayout& L) {
     return (size_t)(p.grid + L.T128) * 16 * 128 * 4 + (((size_t)L.T128 * 8 * 4 + 255) & ~(size_t)255);
 }
 
-template <int WBITS, int NT8, int SPG, bool PARTIALS>
+template <int WBITS, int NT8, int SPG, bool PARTIALS, bool TP>
 static cudaError_t launch_k2(const DecArgs& a, const DecPlan& p, cudaStream_t st) {
-    auto kern = qlinear_decode_kernel<WBITS, NT8, SPG, PARTIALS>;
+    auto kern = qlinear_decode_kernel<WBITS, NT8, SPG, PARTIALS, TP>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);  // + static smem <= 227 KB
         attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -706,9 +736,10 @@ static cudaError_t launch_k2(const DecArgs& a, const DecPlan& p, cudaStream_t st
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <int WBITS, int NT8, bool PARTIALS>
+template <int WBITS, int NT8, bool PARTIALS, bool TP = false>
 static cudaError_t launch_k(const DecArgs& a, const DecPlan& p, cudaStream_t st) {
-    return a.L.G == 64 ? launch_k2<WBITS, NT8, 1, PARTIALS>(a, p, st) : launch_k2<WBITS, NT8, 2, PARTIALS>(a, p, st);
+    return a.L.G == 64 ? launch_k2<WBITS, NT8, 1, PARTIALS, TP>(a, p, st)
+                       : launch_k2<WBITS, NT8, 2, PARTIALS, TP>(a, p, st);
 }
 
 // L2 prefetch of a byte range (the next layer's packed weights): one thread per
@@ -752,7 +783,7 @@ dyq_status_t launch_prefetch_l2(const void* p, size_t bytes, cudaStream_t st) {
 // self-cleaning)] [activation area written by the quantizer kernel].
 dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int M,
                            int m0, const int32_t* row_bits, int bits, void* y, int y_dtype, int32_t* I_out,
-                           void* ws, int64_t* /*err*/, cudaStream_t st) {
+                           void* ws, int64_t* /*err*/, cudaStream_t st, const TpPeers* tp) {
     const int nt8 = dec_nt8(M);
     const ActLayoutDec A = act_layout_dec(L, nt8);
     const DecPlan p = dec_plan(L, nt8);
@@ -783,10 +814,13 @@ dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta
     a.off_x16 = p.off_x16;
     a.trace = g_trace;
     a.serial = g_trace_serial++;
+    a.tp = {};
+    if (tp) a.tp = *tp;
     const bool partials = I_out != nullptr;
     cudaError_t e;
 #define DYQ_DISPATCH(WB)                                                                      \
     if (partials) e = nt8 == 1 ? launch_k<WB, 1, true>(a, p, st) : launch_k<WB, 2, true>(a, p, st); \
+    else if (a.tp.n) e = nt8 == 1 ? launch_k<WB, 1, false, true>(a, p, st) : launch_k<WB, 2, false, true>(a, p, st); \
     else e = nt8 == 1 ? launch_k<WB, 1, false>(a, p, st) : launch_k<WB, 2, false>(a, p, st);
     if (L.wbits == 4) {
         DYQ_DISPATCH(4)

@@ -318,6 +318,40 @@ dyq_status_t dyq_qlinear(const dyq_wdesc_t* wd, const void* codes, const void* m
     return run_decode(L, codes, meta, x, M, row_bits, bits, y, y_dtype, nullptr, workspace, err, (cudaStream_t)stream);
 }
 
+// Fused TP decode: this rank's column shard of y is
+// stored by the decode kernel's epilogue into every rank's full y (peer
+// memory), each 16-column sub-tile announced on every rank's flag.
+dyq_status_t dyq_qlinear_tp(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x,
+                            int32_t M, const int32_t* row_bits, int32_t bits, const dyq_tp_peers_t* peers,
+                            void* workspace, size_t ws_bytes, int64_t* err, dyq_stream_t stream) {
+    if (!peers) return set_error(DYQ_EINVAL, "null peers");
+    if (peers->world < 1 || peers->world > DYQ_TP_MAX || peers->rank < 0 || peers->rank >= peers->world)
+        return set_error(DYQ_EINVAL, "bad rank %d / world %d", peers->rank, peers->world);
+    for (int p = 0; p < peers->world; ++p) {
+        if (!peers->y[p] || !peers->flag[p]) return set_error(DYQ_EINVAL, "null y / flag of rank %d", p);
+        if (!aligned16(peers->y[p])) return set_error(DYQ_EINVAL, "y of rank %d must be 16-byte aligned", p);
+    }
+    WLayout L;
+    dyq_status_t rc = validate_ql(wd, &L, codes, meta, x, M, row_bits, bits, true, 1, true, workspace, ws_bytes);
+    if (rc || M == 0) return rc;
+    if (M > DEC_MPAD || g_path == 2)
+        return set_error(DYQ_EUNSUPPORTED, "fused TP epilogue is decode-only (M = %d > %d): use dyq_tp_allgather",
+                         M, DEC_MPAD);
+    TpPeers tp{};
+    tp.n = peers->world;
+    for (int p = 0; p < tp.n; ++p) {
+        tp.y[p] = peers->y[p];
+        tp.flag[p] = reinterpret_cast<unsigned long long*>(peers->flag[p]);
+    }
+    tp.ldy = peers->world * wd->N;
+    tp.col0 = peers->rank * wd->N;
+    const cudaStream_t st = (cudaStream_t)stream;
+    uint8_t* area = reinterpret_cast<uint8_t*>(workspace) + act_area_offset(L);
+    rc = launch_actquant_dec(L, x, M, 0, row_bits, bits, area, err, st);
+    if (rc) return rc;
+    return launch_decode(L, codes, meta, x, M, 0, row_bits, bits, nullptr, 1, nullptr, workspace, err, st, &tp);
+}
+
 dyq_status_t dyq_qlinear_i32_partials(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x,
                                       int32_t M, const int32_t* row_bits, int32_t bits, int32_t* I, void* workspace,
                                       size_t ws_bytes, int64_t* err, dyq_stream_t stream) {

@@ -71,6 +71,18 @@ __host__ __device__ inline int dec_perm(int kk) {  // kk in [0,64) -> position
     return t * 16 + s * 8 + h * 4 + b;
 }
 
+// Fused tensor-parallel epilogue: the decode kernel
+// stores its column shard straight into every rank's full output y[p]
+// ([M, ldy] bf16, column offset col0) -- peer memory over NVLink, mapped with
+// CUDA IPC -- then release-increments every rank's flag once per 16-column
+// sub-tile.  n = 0: ordinary single-output epilogue.
+constexpr int TP_MAX = 8;
+struct TpPeers {
+    void* y[TP_MAX];
+    unsigned long long* flag[TP_MAX];
+    int n, ldy, col0;
+};
+
 struct ActLayoutDec {
     size_t cp_off, x16_off, zx_off, bytes;
     int nt8, cp_stride, x16_stride;
@@ -252,5 +264,5 @@ dyq_status_t launch_actquant_export(const WLayout& L, int M, const int32_t* row_
 // ws = zero-initialised split-K accumulator area (decode_ws_bytes)
 dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta, const uint16_t* x, int M,
                            int m0, const int32_t* row_bits, int bits, void* y, int y_dtype, int32_t* I_out,
-                           void* ws, int64_t* err, cudaStream_t st);
+                           void* ws, int64_t* err, cudaStream_t st, const TpPeers* tp = nullptr);
 }  // namespace dyq

@@ -1007,7 +1007,7 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
     const dyq_model_desc_t& D = m->d;
     const ModelLayout& L = m->L;
     if (E <= 0 || E > D.E) return set_error(DYQ_EINVAL, "E = %d outside [1, %d]", E, D.E);
-    const int S = L.S, d = D.d, ffn = D.ffn, H = D.n_heads, NL = D.n_layers;
+    const int S = L.S, d = D.d, H = D.n_heads, NL = D.n_layers;
     const int MP = E * S;
     uint16_t* h = m->at<uint16_t>(L.h);
     uint16_t* xn = m->at<uint16_t>(L.xn);

@@ -559,7 +559,6 @@ __global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, i
             vmax = fmaxf(vmax, v[i]);
         }
     }
-#pragma unroll
     bad = warp_min_i(bad);
     if (bad != 0x7fffffff && lane == 0) report_nonfinite(err, (int64_t)m * L.K + (int64_t)g * G + bad);
     if (b != 2 && b != 4 && b != 8) {

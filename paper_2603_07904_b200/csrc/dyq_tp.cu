@@ -14,6 +14,7 @@
 #include <string.h>
 
 #include "dyq_internal.cuh"
+#include "dyq_ptx.cuh"
 
 namespace dyq {
 
@@ -61,11 +62,87 @@ __global__ void tp_interleave_kernel(const uint16_t* __restrict__ buf, int P, in
         *reinterpret_cast<const uint4*>(buf + ((size_t)r * M + m) * Ns + j);
 }
 
+// Wait until *flag >= target (system-scope acquire), bounded: after ~timeout_ns
+// the kernel records a timeout in *status and returns instead of hanging.
+__global__ void tp_wait_kernel(const unsigned long long* flag, unsigned long long target, long long timeout_ns,
+                               int* status) {
+    ptx::pdl_launch_dependents();
+    if (threadIdx.x != 0) return;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+        if (v >= target) return;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if ((long long)(t - t0) > timeout_ns) {
+            if (status) atomicExch(status, 1);
+            return;
+        }
+        __nanosleep(100);
+    }
+}
+
 }  // namespace dyq
 
 using namespace dyq;
 
 extern "C" {
+
+dyq_status_t dyq_tp_wait(const uint64_t* flag, uint64_t target, int32_t* timed_out, dyq_stream_t stream) {
+    if (!flag) return set_error(DYQ_EINVAL, "null flag");
+    tp_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(reinterpret_cast<const unsigned long long*>(flag),
+                                                      (unsigned long long)target, 10'000'000'000LL, timed_out);
+    return check_launch("tp_wait_kernel");
+}
+
+// An IPC handle names a whole allocation (e.g. a caching-allocator segment),
+// so the handle travels with the pointer's offset from the allocation base
+// (cuMemGetAddressRange through the runtime's driver entry point: no link-time
+// libcuda dependency).
+dyq_status_t dyq_ipc_handle(void* dev_ptr, void* handle_out, uint64_t* offset_out) {
+    if (!dev_ptr || !handle_out || !offset_out) return set_error(DYQ_EINVAL, "null pointer");
+    typedef int (*RangeFn)(unsigned long long*, size_t*, unsigned long long);
+    static RangeFn range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &fn, 12000, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<RangeFn>(fn);
+    }();
+    if (!range) return set_error(DYQ_EUNSUPPORTED, "cuMemGetAddressRange entry point unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+        return set_error(DYQ_EINVAL, "pointer is not a device allocation");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (uint64_t)((uintptr_t)dev_ptr - base);
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_ipc_open(const void* handle, uint64_t offset, void** dev_ptr) {
+    if (!handle || !dev_ptr) return set_error(DYQ_EINVAL, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    *dev_ptr = reinterpret_cast<uint8_t*>(base) + offset;
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_ipc_close(void* dev_ptr, uint64_t offset) {
+    if (!dev_ptr) return set_error(DYQ_EINVAL, "null pointer");
+    const cudaError_t e = cudaIpcCloseMemHandle(reinterpret_cast<uint8_t*>(dev_ptr) - offset);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return DYQ_OK;
+}
 
 dyq_status_t dyq_tp_shard(int32_t N, int32_t world, int32_t rank, int32_t* n0, int32_t* n1) {
     if (world <= 0 || rank < 0 || rank >= world) return set_error(DYQ_EINVAL, "bad rank %d / world %d", rank, world);

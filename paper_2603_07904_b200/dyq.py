@@ -59,6 +59,11 @@ _SIGS = {
     "dyq_comm_destroy": [P],
     "dyq_tp_allgather": [P, P, i32, i32, P, P, P],
     "dyq_tp_interleave": [P, i32, i32, i32, P, P],
+    "dyq_qlinear_tp": [P, P, P, P, i32, P, i32, P, P, sz, P, P],
+    "dyq_tp_wait": [P, C.c_uint64, P, P],
+    "dyq_ipc_handle": [P, P, P],
+    "dyq_ipc_open": [P, C.c_uint64, P],
+    "dyq_ipc_close": [P, C.c_uint64],
     "dyq_policy_step_bits": [P, i32, P, P, P, P, P],
     "dyq_calib_collect": [P, P, i32, P, P, P, P, P, P],
     "dyq_calib_errors": [P, i32, i32, P, P],
@@ -88,6 +93,8 @@ def lib():
             raise RuntimeError(f"libdyq.so not built ({LIB_PATH}); run __graft_entry__.build()")
         L = C.CDLL(LIB_PATH)
         for name, args in _SIGS.items():
+            if os.environ.get("DYQ_LIB") and not hasattr(L, name):
+                continue  # older A/B build (tools/): entry points added since are absent
             f = getattr(L, name)
             f.argtypes = args
             f.restype = _RESTYPES.get(name, C.c_int)
@@ -471,6 +478,55 @@ def comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _call("dyq_comm_unique_id", buf)
     return buf.raw
+
+
+TP_MAX = 8
+
+
+class TpPeers(C.Structure):
+    """dyq_tp_peers_t: every rank's full y and arrival flag as mapped here."""
+    _fields_ = [("world", i32), ("rank", i32), ("y", C.c_void_p * TP_MAX), ("flag", C.c_void_p * TP_MAX)]
+
+
+def tp_peers(world: int, rank: int, y_ptrs, flag_ptrs) -> TpPeers:
+    """y_ptrs / flag_ptrs: device addresses (ints) of rank p's buffers, p < world."""
+    t = TpPeers()
+    t.world, t.rank = world, rank
+    for p in range(world):
+        t.y[p] = int(y_ptrs[p])
+        t.flag[p] = int(flag_ptrs[p])
+    return t
+
+
+def qlinear_tp(lin: "PackedLinear", x, M: int, row_bits, bits: int, peers: TpPeers, ws, err=None, stream=None):
+    """Fused TP decode: this rank's shard `lin` (rows dyq_tp_shard) written
+    into every rank's full y; see dyq_qlinear_tp."""
+    _call("dyq_qlinear_tp", C.byref(lin.wd), _ptr(lin.codes), _ptr(lin.meta), _ptr(x), M, _ptr(row_bits), bits,
+          C.byref(peers), _ptr(ws), ws.numel() * ws.element_size(), _ptr(err), _stream(stream))
+
+
+def tp_wait(flag, target: int, timed_out=None, stream=None):
+    """Stream-ordered wait until flag (device uint64 / int64 tensor) >= target."""
+    _call("dyq_tp_wait", _ptr(flag), target, _ptr(timed_out), _stream(stream))
+
+
+def ipc_handle(t) -> tuple[bytes, int]:
+    """(handle, offset) of a device tensor's memory, for dyq_ipc_open in a peer."""
+    buf = C.create_string_buffer(64)
+    off = C.c_uint64(0)
+    _call("dyq_ipc_handle", C.c_void_p(t.data_ptr()), buf, C.byref(off))
+    return buf.raw, off.value
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    h = C.create_string_buffer(handle, 64)
+    p = C.c_void_p()
+    _call("dyq_ipc_open", h, offset, C.byref(p))
+    return p.value
+
+
+def ipc_close(ptr: int, offset: int):
+    _call("dyq_ipc_close", C.c_void_p(ptr), offset)
 
 
 class Comm:

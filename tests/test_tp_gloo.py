@@ -78,3 +78,23 @@ def test_two_rank_column_sharded_qlinear_is_exact(tmp_path, bits):
     y, I = oracle.qlinear(x, oracle.pack_weights(W, 64, 4), 64, bits, want_I=True)
     assert np.array_equal(np.load(tmp_path / "y.npy"), y)
     assert np.array_equal(np.load(tmp_path / "I.npy"), I)
+
+
+def test_fused_tp_peers_struct_and_validation():
+    """dyq_tp_peers_t layout (include/dyq.h) and dyq_qlinear_tp's host-side
+    argument checks, which run before any CUDA call."""
+    import ctypes as C
+    from paper_2603_07904_b200 import dyq
+    assert C.sizeof(dyq.TpPeers) == 8 + 8 * 8 + 8 * 8
+    assert dyq.TpPeers.y.offset == 8 and dyq.TpPeers.flag.offset == 72
+    t = dyq.tp_peers(2, 1, [0x1000, 0x2000], [0x3000, 0x4000])
+    assert (t.world, t.rank, t.y[1], t.flag[0]) == (2, 1, 0x2000, 0x3000)
+    L = dyq.lib()
+    wd = dyq.WDesc(256, 256, 64, 4, 0)
+    assert L.dyq_qlinear_tp(C.byref(wd), None, None, None, 1, None, 4, None, None, 0, None, None) == 1
+    bad = dyq.tp_peers(1, 0, [0x1000], [0x2000])
+    bad.world = 9  # > DYQ_TP_MAX
+    assert L.dyq_qlinear_tp(C.byref(wd), None, None, None, 1, None, 4, C.byref(bad), None, 0, None, None) == 1
+    bad = dyq.tp_peers(2, 0, [0x1000, 0], [0x2000, 0x3000])  # null y of rank 1
+    assert L.dyq_qlinear_tp(C.byref(wd), None, None, None, 1, None, 4, C.byref(bad), None, 0, None, None) == 1
+    assert b"rank 1" in L.dyq_last_error()
