@@ -585,54 +585,65 @@ def main():
     # launches, D2H of the step's result (block output y and b*), per step
     e2e = None
     if not args.profile:
-        x_host = [[xs[s][li].cpu().pin_memory() for li in range(len(lins))] for s in range(8)]
-        a_host = acts.cpu().pin_memory()
-        x_dev = [torch.empty_like(xs[0][li]) for li in range(len(lins))]
-        a_dev = torch.empty(1, 7, dtype=torch.float32, device=dev)
-        y_host = torch.empty(M, lins[-1][1], dtype=torch.bfloat16).pin_memory()
-        b_host = torch.empty(1, dtype=torch.int32).pin_memory()
-        h2d = sum(x.numel() * 2 for x in x_host[0]) + 28
-        d2h = y_host.numel() * 2 + 4
+        # one pinned staging buffer per step index k = t % 8: [a_{t-1} (7 f32,
+        # padded to 64 B) | x_qkv | x_o | x_gate_up | x_down] (bf16 bits), one H2D
+        # copy per step into the same layout on the device; the step's result
+        # [y_down | b*] comes back in one D2H copy
+        HP = 32  # int16 elements of the action header (64 B)
+        sizes = [xs[0][li].numel() for li in range(len(lins))]
+        offs = [HP + sum(sizes[:li]) for li in range(len(lins))]
+        tot = HP + sum(sizes)
+        in_host = []
+        for k in range(8):
+            hb = torch.zeros(tot, dtype=torch.int16).pin_memory()
+            for li in range(len(lins)):
+                hb[offs[li]:offs[li] + sizes[li]] = xs[k][li].reshape(-1).view(torch.int16).cpu()
+            in_host.append(hb)
+        in_dev = torch.empty(tot, dtype=torch.int16, device=dev)
+        a_dev = in_dev[:14].view(torch.float32).view(1, 7)
+        x_dev = [in_dev[offs[li]:offs[li] + sizes[li]].view(torch.bfloat16).view(xs[0][li].shape)
+                 for li in range(len(lins))]
+        n_last = lins[-1][1]
+        out_dev = torch.empty(M * n_last + 2, dtype=torch.int16, device=dev)
+        y_dev = out_dev[:M * n_last].view(torch.bfloat16).view(M, n_last)
+        b_dev = out_dev[M * n_last:].view(torch.int32)
+        out_host = torch.empty_like(out_dev, device="cpu").pin_memory()
+        a_host = acts.cpu()
+        h2d = tot * 2
+        d2h = out_host.numel() * 2
         n_e2e = min(args.steps, 200)
+
+        def e2e_step(k, stream=None):
+            in_dev.copy_(in_host[k], non_blocking=True)
+            dyq.select_route(state, 1, a_dev, b_dev, M, row_bits, stream=stream)
+            for li, (name, N, K) in enumerate(lins):
+                p = packed[k % C][li]
+                yo = y_dev if li == len(lins) - 1 else ys[li]
+                dyq.qlinear(p.wd, p.codes, p.meta, x_dev[li], M, row_bits, 0, yo, 1, wss[li], stream=stream)
+            out_host.copy_(out_dev, non_blocking=True)
+
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         tc = time.perf_counter()
         for i in range(n_e2e):
             t = t_cur + args.steps + i
-            a_dev.copy_(a_host[t - 1], non_blocking=True)
-            for li in range(len(lins)):
-                x_dev[li].copy_(x_host[t % 8][li], non_blocking=True)
-            dyq.select_route(state, 1, a_dev, bits, M, row_bits)
-            for li, (name, N, K) in enumerate(lins):
-                p = packed[t % C][li]
-                dyq.qlinear(p.wd, p.codes, p.meta, x_dev[li], M, row_bits, 0, ys[li], 1, wss[li])
-            y_host.copy_(ys[-1], non_blocking=True)
-            b_host.copy_(bits, non_blocking=True)
+            in_host[t % 8][:14].view(torch.float32).copy_(a_host[t - 1].reshape(-1))
+            e2e_step(t % 8)
             torch.cuda.current_stream().synchronize()
         dt_eager = episodes.max_over_ranks((time.perf_counter() - tc) / n_e2e, device=dev)
-        # the same public-API step captured as a CUDA graph, one per step index
-        # k = t % 8 (input set k from its pinned buffers, weight copy k % C):
-        # pinned H2D of the step's inputs, select_route, 4 x dyq_qlinear, D2H of
-        # y and b*.  Per step the host writes a_{t-1} into a pinned staging
-        # buffer (28 B), replays graph t % 8 and waits for the result.
+        # the same public-API step captured as a CUDA graph, one per step index k
+        # (input set k, weight copy k % C): H2D of the staging buffer,
+        # select_route, 4 x dyq_qlinear, D2H of [y | b*].  Per step the host
+        # writes a_{t-1} into staging buffer t % 8, replays graph t % 8 and waits.
         assert 8 % C == 0 or C % 8 == 0
-        a_stage = torch.empty(1, 7, dtype=torch.float32).pin_memory()
         se = torch.cuda.Stream()
         graphs = []
         for k in range(8):
             ge = torch.cuda.CUDAGraph()
             se.wait_stream(torch.cuda.current_stream())
             with torch.cuda.graph(ge, stream=se):
-                a_dev.copy_(a_stage, non_blocking=True)
-                for li in range(len(lins)):
-                    x_dev[li].copy_(x_host[k][li], non_blocking=True)
-                dyq.select_route(state, 1, a_dev, bits, M, row_bits, stream=se)
-                for li, (name, N, K) in enumerate(lins):
-                    p = packed[k % C][li]
-                    dyq.qlinear(p.wd, p.codes, p.meta, x_dev[li], M, row_bits, 0, ys[li], 1, wss[li], stream=se)
-                y_host.copy_(ys[-1], non_blocking=True)
-                b_host.copy_(bits, non_blocking=True)
+                e2e_step(k, stream=se)
             graphs.append(ge)
         torch.cuda.synchronize()
         t_e = t_cur + args.steps + n_e2e
@@ -642,7 +653,7 @@ def main():
         tc = time.perf_counter()
         for i in range(n_e2e):
             t = t_e + i
-            a_stage.copy_(a_host[t - 1])
+            in_host[t % 8][:14].view(torch.float32).copy_(a_host[t - 1].reshape(-1))
             graphs[t % 8].replay()  # enqueued on the current stream
             torch.cuda.current_stream().synchronize()
         dt = episodes.max_over_ranks((time.perf_counter() - tc) / n_e2e, device=dev)
@@ -651,11 +662,11 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(dt * 1e3, 4), "steps": n_e2e,
                "path": "public API (select_route + 4 x dyq_qlinear) captured per step index in a CUDA graph with "
-                       "the pinned H2D input copies and the D2H of y and b*; per step: host writes a_{t-1} into a "
-                       "pinned staging buffer, graph replay, stream sync",
+                       "one pinned H2D copy of the step's inputs [a_{t-1} | x x 4] and one D2H copy of [y | b*]; "
+                       "per step: host writes a_{t-1} into the pinned staging buffer, graph replay, stream sync",
                "eager": {"value": round(bytes_step * world / dt_eager / 1e9, 2),
                          "ms_per_step": round(dt_eager * 1e3, 4),
-                         "path": "eager dyq_* calls via the Python binding, pinned H2D in, D2H out, sync per step"}}
+                         "path": "eager dyq_* calls via the Python binding, same staging buffers, sync per step"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
