@@ -148,6 +148,12 @@ __global__ void __launch_bounds__(SEL_THREADS) select_bits_kernel(uint8_t* state
     const int e = blockIdx.x;
     ptx::pdl_wait();  // state and a_{t-1} come from the preceding kernels
     ptx::pdl_launch_dependents();
+    const bool observe = prev_action != nullptr;
+    float act[6];
+    if (observe && threadIdx.x == 0) {  // issued first: its latency overlaps the state copy
+#pragma unroll
+        for (int i = 0; i < 6; ++i) act[i] = prev_action[(size_t)e * 7 + i];
+    }
     {
         const uint4* src = reinterpret_cast<const uint4*>(state);
         uint4* dst = reinterpret_cast<uint4*>(ssm);
@@ -168,12 +174,6 @@ __global__ void __launch_bounds__(SEL_THREADS) select_bits_kernel(uint8_t* state
     double* smag = reinterpret_cast<double*>(base + h.off_smag);
     double* sjerk = reinterpret_cast<double*>(base + h.off_sjerk);
     int32_t* I = reinterpret_cast<int32_t*>(base + h.off_int);
-    const bool observe = prev_action != nullptr;
-    float act[6];
-    if (observe && threadIdx.x == 0) {
-#pragma unroll
-        for (int i = 0; i < 6; ++i) act[i] = prev_action[(size_t)e * 7 + i];
-    }
     __syncthreads();
 
     if (observe) {
