@@ -134,3 +134,43 @@ def test_policy_step_and_calibration_openvla_shapes():
         ref = np.stack([oc.action_error(a[(j + 1) * Ec:(j + 2) * Ec], a[:Ec]) for j in range(3)], axis=1)
         np.testing.assert_allclose(err.cpu().numpy(), ref, rtol=1e-15, atol=0)
         prev = a[:Ec].copy()
+
+
+@pytest.mark.parametrize("name,N,K", [l for l in synth.LLAMA_BLOCK_LINEARS if l[0] in ("gate_up", "down")],
+                         ids=["gate_up", "down"])
+@pytest.mark.parametrize("mode", [4, "mixed"])
+def test_prefill_eight_episodes_sampled(name, N, K, mode):
+    """Largest prefill of the policy slice: E = 8 episodes x 288 tokens = 2304
+    rows (18 full 128-token tiles of the tcgen05 kernel)."""
+    M = 8 * 288
+    seed = zlib.crc32(f"{name}/E8/{mode}".encode()) % 1000
+    w = synth.weights_bf16_torch(N, K, seed=1 + seed, device=DEV)
+    x = synth.activations_bf16_torch(M, K, seed=1000 + seed, device=DEV)
+    lin = dyq.PackedLinear.from_bf16(w, group=G, wbits=WB)
+    rows = _rows(N, seed)[::2]
+    w_rows = w[torch.from_numpy(rows).to(DEV)].cpu().numpy().view(np.uint16)
+    del w
+    rb = _rowbits(M, mode)
+    y = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=DEV)
+    dyq.qlinear(lin.wd, lin.codes, lin.meta, x, M, torch.from_numpy(rb).to(DEV), 0, y, 1, lin.workspace(M))
+    yref, _ = oracle.qlinear(x.cpu().numpy().view(np.uint16), oracle.pack_weights(w_rows, G, WB), G, rb)
+    got = y.float().cpu().numpy()
+    assert not np.isnan(got).any()
+    check_close(got[:, rows], yref, 2e-2)
+
+
+def test_empty_inputs_are_noops():
+    """M = 0 (no tokens) is valid for every linear entry point and writes nothing."""
+    N, K = 256, 256
+    lin = dyq.PackedLinear.from_bf16(synth.weights_bf16_torch(N, K, seed=3, device=DEV), group=G, wbits=WB)
+    x = torch.zeros(1, K, dtype=torch.int16, device=DEV)
+    y = torch.full((1, N), 7.0, dtype=torch.float32, device=DEV)
+    ws = lin.workspace(1)
+    dyq.qlinear(lin.wd, lin.codes, lin.meta, x, 0, None, 4, y, 0, ws)
+    I = torch.full((1, N, K // G), 5, dtype=torch.int32, device=DEV)
+    dyq.qlinear_i32_partials(lin.wd, lin.codes, lin.meta, x, 0, None, 4, I, ws)
+    f = torch.zeros(1, dtype=torch.int64, device=DEV)
+    yb = torch.full((1, N), 3, dtype=torch.int16, device=DEV)
+    dyq.qlinear_tp(lin, x, 0, None, 4, dyq.tp_peers(1, 0, [yb.data_ptr()], [f.data_ptr()]), ws)
+    torch.cuda.synchronize()
+    assert bool((y == 7.0).all()) and bool((I == 5).all()) and bool((yb == 3).all()) and int(f.item()) == 0
