@@ -337,12 +337,13 @@ DYQ_API dyq_status_t dyq_tp_interleave(const uint16_t* buf, int32_t P, int32_t M
  * epilogue stores y[:, r Ns + j] (bf16) straight into EVERY rank's full output
  * y[p] ([M, world * Ns], peer memory over NVLink / NVSwitch, mapped with
  * dyq_ipc_open); each CTA then fences at system scope and adds the number of
- * 16-column sub-tiles it wrote to every rank's flag[p] (Ns / 16 per call in
- * total).  After the c-th call on every rank, each flag
- * reaches c * world * Ns / 16 = c * N / 16; dyq_tp_wait orders a rank's stream
- * after that point.  Consecutive calls must alternate between two y buffers
- * (a peer may start call c+1 while this rank still reads call c's output).
- * Decode only (M <= 16; DYQ_EUNSUPPORTED above: use dyq_tp_allgather).
+ * 16-column sub-tiles it wrote to every rank's flag[p].  One call adds
+ * dyq_tp_flag_delta(N, M) to every flag once all ranks' parts have landed
+ * (N / 16 for decode, M <= 16; N / 16 per 144-token tile for the tcgen05
+ * prefill path); dyq_tp_wait orders a rank's stream after the running total.
+ * Consecutive calls must alternate between two y buffers (a peer may start
+ * call c+1 while this rank still reads call c's output).  Both regimes:
+ * decode (M <= 16, one launch) and prefill (M > 16).
  * wd = this rank's shard descriptor (N = Ns, dyq_tp_shard rows). */
 #define DYQ_TP_MAX 8
 typedef struct {
@@ -354,6 +355,8 @@ DYQ_API dyq_status_t dyq_qlinear_tp(const dyq_wdesc_t* wd, const void* codes, co
                                     const uint16_t* x, int32_t M, const int32_t* row_bits, int32_t bits,
                                     const dyq_tp_peers_t* peers, void* workspace, size_t ws_bytes,
                                     int64_t* err, dyq_stream_t stream);
+/* Per-call flag increment of dyq_qlinear_tp for full width N and M tokens. */
+DYQ_API dyq_status_t dyq_tp_flag_delta(int32_t N, int32_t M, uint64_t* delta);
 /* Stream-ordered wait until *flag >= target (device u64, ld.acquire.sys).
  * Bounded: after 10 s the kernel sets *timed_out = 1 (device int32, may be
  * NULL) and returns rather than hang the GPU. */

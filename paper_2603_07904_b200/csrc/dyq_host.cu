@@ -334,9 +334,6 @@ dyq_status_t dyq_qlinear_tp(const dyq_wdesc_t* wd, const void* codes, const void
     WLayout L;
     dyq_status_t rc = validate_ql(wd, &L, codes, meta, x, M, row_bits, bits, true, 1, true, workspace, ws_bytes);
     if (rc || M == 0) return rc;
-    if (M > DEC_MPAD || g_path == 2)
-        return set_error(DYQ_EUNSUPPORTED, "fused TP epilogue is decode-only (M = %d > %d): use dyq_tp_allgather",
-                         M, DEC_MPAD);
     TpPeers tp{};
     tp.n = peers->world;
     for (int p = 0; p < tp.n; ++p) {
@@ -346,10 +343,28 @@ dyq_status_t dyq_qlinear_tp(const dyq_wdesc_t* wd, const void* codes, const void
     tp.ldy = peers->world * wd->N;
     tp.col0 = peers->rank * wd->N;
     const cudaStream_t st = (cudaStream_t)stream;
+    const bool prefill = g_path == 2 || (g_path == 0 && M > DEC_MPAD);  // as run_decode
+    if (!prefill && M > DEC_MPAD)
+        return set_error(DYQ_EUNSUPPORTED, "fused TP decode handles M <= %d per call (M = %d)", DEC_MPAD, M);
+    if (prefill) {  // tcgen05 kernel, TP epilogue per (tile, token tile) CTA
+        uint8_t* pa = reinterpret_cast<uint8_t*>(workspace) + prefill_area_offset(L);
+        rc = launch_actquant_pre(L, x, M, row_bits, bits, pa, err, st);
+        if (rc) return rc;
+        return launch_prefill(L, codes, meta, M, row_bits, bits, nullptr, 1, nullptr, pa, st, &tp);
+    }
     uint8_t* area = reinterpret_cast<uint8_t*>(workspace) + act_area_offset(L);
     rc = launch_actquant_dec(L, x, M, 0, row_bits, bits, area, err, st);
     if (rc) return rc;
     return launch_decode(L, codes, meta, x, M, 0, row_bits, bits, nullptr, 1, nullptr, workspace, err, st, &tp);
+}
+
+dyq_status_t dyq_tp_flag_delta(int32_t N, int32_t M, uint64_t* delta) {
+    if (!delta) return set_error(DYQ_EINVAL, "null delta");
+    if (N <= 0 || N % 16 || M < 0) return set_error(DYQ_ESHAPE, "N = %d, M = %d", N, M);
+    const bool prefill = g_path == 2 || (g_path == 0 && M > DEC_MPAD);
+    const int tiles = (M == 0) ? 0 : (prefill ? (M + PRE_PT - 1) / PRE_PT : 1);
+    *delta = (uint64_t)(N / 16) * (uint64_t)tiles;
+    return DYQ_OK;
 }
 
 dyq_status_t dyq_qlinear_i32_partials(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x,

@@ -77,6 +77,7 @@ __host__ __device__ inline int dec_perm(int kk) {  // kk in [0,64) -> position
 // CUDA IPC -- then release-increments every rank's flag once per 16-column
 // sub-tile.  n = 0: ordinary single-output epilogue.
 constexpr int TP_MAX = 8;
+constexpr int PRE_PT = 144;  // prefill token tile (dyq_prefill.cu PT): flag increments per call
 struct TpPeers {
     void* y[TP_MAX];
     unsigned long long* flag[TP_MAX];
@@ -226,7 +227,7 @@ PreActLayout pre_act_layout(const WLayout& L, int M);
 dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, const int32_t* row_bits, int bits,
                                  void* act, int64_t* err, cudaStream_t st, int gated = 0);
 dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,
-                            int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st);
+                            int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st, const TpPeers* tp = nullptr);
 extern int g_path;
 // dyq_select.cu
 size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);

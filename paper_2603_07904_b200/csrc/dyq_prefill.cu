@@ -62,6 +62,7 @@
 namespace dyq {
 
 constexpr int PT = 144;  // tokens per token tile (MMA N)
+static_assert(PT == PRE_PT, "dyq_tp_flag_delta counts prefill token tiles");
 constexpr int PRE_WARPS = 14;
 constexpr int PRE_THREADS = PRE_WARPS * 32;
 constexpr int PAR_BYTES = PT * 4;  // per (tile, group): float s_x[144] (1 for A16 tokens, 0 for absent)
@@ -85,6 +86,7 @@ struct PreArgs {
     PreActLayout P;
     int stages, stage_bytes;
     int off_meta, off_b, off_par, off_a;
+    TpPeers tp;  // fused TP epilogue (TP instantiation only)
 };
 
 __device__ __forceinline__ int token_bits(const PreArgs& a, int m) { return a.row_bits ? a.row_bits[m] : a.bits; }
@@ -97,7 +99,7 @@ __device__ __forceinline__ uint8_t e4m3_of(float v) {  // exact for integers |v|
     return (uint8_t)__nv_cvt_float_to_fp8(v, __NV_SATFINITE, __NV_E4M3);
 }
 
-template <int WBITS, int SPG, bool PARTIALS>
+template <int WBITS, int SPG, bool PARTIALS, bool TP>
 __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const PreArgs a) {
     constexpr int G = SPG * 64;
     constexpr int KSTEPS = G / 16;         // bf16 MMA K steps per group
@@ -485,7 +487,21 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 if (part >= valid || s_col[c] == 0) continue;
                 const size_t m = (size_t)tt * PT + c;
                 const uint4 v = *reinterpret_cast<const uint4*>(stage0 + c * rowp + part * 16);
-                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.y) + (m * L.N + tile * 128) * es + part * 16) = v;
+                if constexpr (TP) {  // bf16 into every rank's full y, this rank's columns
+                    const size_t o = (m * a.tp.ldy + a.tp.col0 + tile * 128) * 2 + part * 16;
+                    for (int p = 0; p < a.tp.n; ++p)
+                        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.tp.y[p]) + o) = v;
+                } else {
+                    *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.y) + (m * L.N + tile * 128) * es + part * 16) =
+                        v;
+                }
+            }
+            if constexpr (TP) {  // announce this CTA's nsub sub-tiles (see dec_tp_announce)
+                ptx::named_bar_sync(1, 256);
+                if (threadIdx.x == PR_WARP0 * 32) {
+                    __threadfence_system();
+                    for (int p = 0; p < a.tp.n; ++p) atomicAdd_system(a.tp.flag[p], (unsigned long long)nsub);
+                }
             }
         }
     }
@@ -637,7 +653,7 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
     return check_launch("actquant_pre_kernel");
 }
 
-template <int WBITS, int SPG, bool PARTIALS>
+template <int WBITS, int SPG, bool PARTIALS, bool TP = false>
 static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
     PreArgs a = a0;
     constexpr int G = SPG * 64;
@@ -652,7 +668,7 @@ static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
     if (a.stages > 8) a.stages = 8;
     if (a.stages < 2) a.stages = 2;
     const size_t smem = 1024 + (size_t)a.stages * a.stage_bytes;
-    auto kern = qlinear_prefill_kernel<WBITS, SPG, PARTIALS>;
+    auto kern = qlinear_prefill_kernel<WBITS, SPG, PARTIALS, TP>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -671,15 +687,16 @@ static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <bool PARTIALS>
+template <bool PARTIALS, bool TP = false>
 static cudaError_t pre_dispatch(const PreArgs& a, dim3 grid, cudaStream_t st) {
     if (a.L.wbits == 4)
-        return a.L.G == 64 ? pre_launch<4, 1, PARTIALS>(a, grid, st) : pre_launch<4, 2, PARTIALS>(a, grid, st);
-    return a.L.G == 64 ? pre_launch<8, 1, PARTIALS>(a, grid, st) : pre_launch<8, 2, PARTIALS>(a, grid, st);
+        return a.L.G == 64 ? pre_launch<4, 1, PARTIALS, TP>(a, grid, st) : pre_launch<4, 2, PARTIALS, TP>(a, grid, st);
+    return a.L.G == 64 ? pre_launch<8, 1, PARTIALS, TP>(a, grid, st) : pre_launch<8, 2, PARTIALS, TP>(a, grid, st);
 }
 
 dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,
-                            int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st) {
+                            int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st,
+                            const TpPeers* tp) {
     PreArgs a;
     a.L = L;
     a.codes = reinterpret_cast<const uint8_t*>(codes);
@@ -694,8 +711,12 @@ dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* met
     a.P = pre_act_layout(L, M);
     a.e4m3 = pre_e4m3_enabled(L) ? 1 : 0;
     a.trace = g_trace;
+    a.tp = {};
+    if (tp) a.tp = *tp;
     const dim3 grid(L.T128, (M + PT - 1) / PT);
-    const cudaError_t e = I_out ? pre_dispatch<true>(a, grid, st) : pre_dispatch<false>(a, grid, st);
+    const cudaError_t e = I_out ? pre_dispatch<true>(a, grid, st)
+                          : tp  ? pre_dispatch<false, true>(a, grid, st)
+                                : pre_dispatch<false>(a, grid, st);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "qlinear_prefill_kernel launch: %s", cudaGetErrorString(e));
     return DYQ_OK;
 }

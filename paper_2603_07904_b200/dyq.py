@@ -61,6 +61,7 @@ _SIGS = {
     "dyq_tp_interleave": [P, i32, i32, i32, P, P],
     "dyq_qlinear_tp": [P, P, P, P, i32, P, i32, P, P, sz, P, P],
     "dyq_tp_wait": [P, C.c_uint64, P, P],
+    "dyq_tp_flag_delta": [i32, i32, P],
     "dyq_ipc_handle": [P, P, P],
     "dyq_ipc_open": [P, C.c_uint64, P],
     "dyq_ipc_close": [P, C.c_uint64],
@@ -503,6 +504,13 @@ def qlinear_tp(lin: "PackedLinear", x, M: int, row_bits, bits: int, peers: TpPee
     into every rank's full y; see dyq_qlinear_tp."""
     _call("dyq_qlinear_tp", C.byref(lin.wd), _ptr(lin.codes), _ptr(lin.meta), _ptr(x), M, _ptr(row_bits), bits,
           C.byref(peers), _ptr(ws), ws.numel() * ws.element_size(), _ptr(err), _stream(stream))
+
+
+def tp_flag_delta(N: int, M: int) -> int:
+    """Per-call flag increment of qlinear_tp (full width N, M tokens)."""
+    d = C.c_uint64(0)
+    _call("dyq_tp_flag_delta", N, M, C.byref(d))
+    return d.value
 
 
 def tp_wait(flag, target: int, timed_out=None, stream=None):

@@ -8,7 +8,7 @@ import torch.distributed as dist
 import synth
 from paper_2603_07904_b200 import dyq
 
-N, K, M = 1024, 512, 8
+N, K, M, MP = 1024, 512, 8, 160  # MP > 16: the tcgen05 prefill path (two token tiles)
 HDR = 256  # flag lives in the first bytes of the rank's buffer
 
 
@@ -27,10 +27,11 @@ def worker(rank, world, port):
     dev = "cuda:0"
     W = torch.from_numpy(synth.weights_bf16(N, K, seed=41).view(np.int16)).to(dev)
     x = torch.from_numpy(synth.activations_bf16(M, K, seed=42).view(np.int16)).to(dev)
+    xp = torch.from_numpy(synth.activations_bf16(MP, K, seed=43).view(np.int16)).to(dev)
     a, b = dyq.tp_shard(N, world, rank)
     lin = dyq.PackedLinear.from_bf16(W[a:b].contiguous(), group=64, wbits=4)
-    ws = lin.workspace(M)
-    ybytes = M * N * 2
+    ws = lin.workspace(MP)
+    ybytes = MP * N * 2
     buf = torch.zeros(HDR + 2 * ybytes, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
     h, off = dyq.ipc_handle(buf)
@@ -47,16 +48,19 @@ def worker(rank, world, port):
     flag = buf[:8].view(torch.int64)
     timed_out = torch.zeros(1, dtype=torch.int32, device=dev)
     dist.barrier()
-    for c, bits in enumerate([2, 4, 16, 8], start=1):
+    target = 0
+    for c, (bits, m) in enumerate([(2, M), (4, M), (16, MP), (8, M), (4, MP)], start=1):
         s = (c - 1) % 2
+        xm = x if m == M else xp
         peers = dyq.tp_peers(world, rank, [q + HDR + s * ybytes for q in base], base)
-        dyq.qlinear_tp(lin, x, M, None, bits, peers, ws)
-        dyq.tp_wait(flag, c * N // 16, timed_out)
+        dyq.qlinear_tp(lin, xm, m, None, bits, peers, ws)
+        target += dyq.tp_flag_delta(N, m)
+        dyq.tp_wait(flag, target, timed_out)
         torch.cuda.synchronize()
         assert int(timed_out.item()) == 0, f"rank {rank}: wait timed out at call {c}"
-        assert int(flag.item()) == c * N // 16, (rank, c, int(flag.item()))
-        y = buf[HDR + s * ybytes:HDR + (s + 1) * ybytes].view(torch.int16).view(M, N)
-        ref = shard_refs(W, x, world, bits)
+        assert int(flag.item()) == target, (rank, c, int(flag.item()))
+        y = buf[HDR + s * ybytes:HDR + s * ybytes + m * N * 2].view(torch.int16).view(m, N)
+        ref = shard_refs(W, xm, world, bits)
         assert torch.equal(y, ref), f"rank {rank} call {c}: fused TP output differs"
     dist.barrier()
     for ptr, o in opened:

@@ -22,7 +22,8 @@ from paper_2603_07904_b200 import dyq  # noqa: E402
 DEV = "cuda:0"
 
 
-@pytest.mark.parametrize("P,M,N", [(1, 1, 512), (2, 8, 1024), (4, 16, 2048), (8, 3, 1024), (2, 5, 22016)])
+@pytest.mark.parametrize("P,M,N", [(1, 1, 512), (2, 8, 1024), (4, 16, 2048), (8, 3, 1024), (2, 5, 22016),
+                                   (2, 17, 1024), (4, 288, 2048), (8, 40, 1024)])
 def test_fused_simulated_ranks(P, M, N):
     K = 512
     W = torch.from_numpy(synth.weights_bf16(N, K, seed=N + P).view(np.int16)).to(DEV)
@@ -36,23 +37,25 @@ def test_fused_simulated_ranks(P, M, N):
     flags = [torch.zeros(1, dtype=torch.int64, device=DEV) for _ in range(P)]
     to = torch.zeros(1, dtype=torch.int32, device=DEV)
     rb = torch.tensor([[2, 4, 8, 16][m % 4] for m in range(M)], dtype=torch.int32, device=DEV)
+    delta = dyq.tp_flag_delta(N, M)
+    assert delta == N // 16 * (1 if M <= 16 else -(-M // 144))
     for c, (bits, row_bits) in enumerate([(4, None), (2, None), (0, rb), (16, None)], start=1):
         s = (c - 1) % 2
         for r in range(P):
             peers = dyq.tp_peers(P, r, [t.data_ptr() for t in ys[s]], [f.data_ptr() for f in flags])
             dyq.qlinear_tp(lins[r], x, M, row_bits, bits, peers, wss[r])
         for r in range(P):
-            dyq.tp_wait(flags[r], c * N // 16, to)
+            dyq.tp_wait(flags[r], c * delta, to)
         torch.cuda.synchronize()
         assert int(to.item()) == 0
-        assert [int(f.item()) for f in flags] == [c * N // 16] * P
+        assert [int(f.item()) for f in flags] == [c * delta] * P
         ref = torch.cat([lin(x, row_bits=row_bits, bits=bits, out_dtype=torch.bfloat16) for lin in lins],
                         dim=1).view(torch.int16)
         for r in range(P):
             assert torch.equal(ys[s][r], ref), (c, r)
 
 
-def test_fused_rejects_prefill_and_bad_peers():
+def test_fused_rejects_bad_peers_and_forced_decode_over_16():
     N, K, M = 256, 256, 20
     W = torch.from_numpy(synth.weights_bf16(N, K, seed=1).view(np.int16)).to(DEV)
     lin = dyq.PackedLinear.from_bf16(W, group=64, wbits=4)
@@ -61,9 +64,13 @@ def test_fused_rejects_prefill_and_bad_peers():
     y = torch.zeros(M, N, dtype=torch.int16, device=DEV)
     f = torch.zeros(1, dtype=torch.int64, device=DEV)
     peers = dyq.tp_peers(1, 0, [y.data_ptr()], [f.data_ptr()])
-    with pytest.raises(dyq.DyqError) as e:
-        dyq.qlinear_tp(lin, x, M, None, 4, peers, ws)
-    assert e.value.code == 3  # DYQ_EUNSUPPORTED: decode only
+    dyq.set_path(1)  # force the decode kernel: one fused launch covers at most 16 rows
+    try:
+        with pytest.raises(dyq.DyqError) as e:
+            dyq.qlinear_tp(lin, x, M, None, 4, peers, ws)
+        assert e.value.code == 3  # DYQ_EUNSUPPORTED
+    finally:
+        dyq.set_path(0)
     bad = dyq.tp_peers(2, 1, [y.data_ptr(), 0], [f.data_ptr(), f.data_ptr()])
     with pytest.raises(dyq.DyqError):
         dyq.qlinear_tp(lin, x, 4, None, 4, bad, ws)
