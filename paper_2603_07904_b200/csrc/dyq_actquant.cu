@@ -5,6 +5,10 @@
 #include "dyq_internal.cuh"
 #include "dyq_ptx.cuh"
 
+#ifndef DYQ_AQ_THREADS
+#define DYQ_AQ_THREADS 512  // threads per act-quant CTA (one warp per (group, token)); 512 measured best
+#endif
+
 namespace dyq {
 
 // One warp per (group g, token m); M <= DEC_MPAD tokens starting at row m0,
@@ -100,8 +104,8 @@ dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int
     const ActLayoutDec A = act_layout_dec(L, dec_nt8(M));
     const int warps = 8 * A.nt8 * L.NG;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((warps * 32 + 255) / 256);
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3((warps * 32 + DYQ_AQ_THREADS - 1) / DYQ_AQ_THREADS);
+    cfg.blockDim = dim3(DYQ_AQ_THREADS);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
