@@ -103,8 +103,11 @@ __device__ inline int phi_dev(double S, double t24, double t48) {
     return 8;
 }
 
-constexpr int SEL_THREADS = 256;
-constexpr int SEL_PER = 4;  // H <= 1024 = SEL_THREADS * SEL_PER
+#ifndef DYQ_SEL_THREADS
+#define DYQ_SEL_THREADS 1024  // one history slot per thread (H <= 1024); step A/B: 256 60.0, 512 59.5, 1024 59.3 us
+#endif
+constexpr int SEL_THREADS = DYQ_SEL_THREADS;
+constexpr int SEL_PER = 1024 / SEL_THREADS;  // H <= 1024 = SEL_THREADS * SEL_PER
 
 // Sorted-multiset update of srt[0..n): delete one copy of `old` (when full),
 // insert x.  All threads of the CTA call it; srt lives in shared memory.
