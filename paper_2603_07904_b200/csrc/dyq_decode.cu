@@ -682,10 +682,11 @@ static int env_int(const char* name, int dflt) {
 static DecPlan dec_plan(const WLayout& L, int nt8) {
     DecPlan p;
     const int unit_codes = (L.G / 64) * 8 * L.chunk;  // full tile
-    // Stage code bytes: 48 KB measured best for the bench step (B200, M = 8:
-    // 61.3 us/step vs 62.4 at 32 KB and 62.5 at 64 KB); halved until at least
-    // two stages fit the shared-memory budget.
-    static const int stage_code_kb = env_int("DYQ_DEC_STAGE_KB", 48);
+    // Stage code bytes: 56 KB (14 W4 groups) measured best for the bench step
+    // (B200, M = 8, same-box sweep: 32 KB 59.35, 40 59.56, 48 59.27, 52 58.62,
+    // 56 58.07, 60 60.48, 64 59.41 us/step); halved until at least two stages
+    // fit the shared-memory budget.
+    static const int stage_code_kb = env_int("DYQ_DEC_STAGE_KB", 56);
     static const int smem_kb1 = env_int("DYQ_DEC_SMEM_KB", 113);
     const int smem_kb = (nt8 == 1 && DEC_CWARPS == 8) ? smem_kb1 : 200;
     const int cps = nt8 * 8 * L.G + nt8 * 64, x16s = nt8 * 8 * L.G * 2;
