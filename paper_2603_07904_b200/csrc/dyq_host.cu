@@ -234,7 +234,12 @@ dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* byt
     if (rc) return rc;
     if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range [0, 65536]");
     if (!bytes) return set_error(DYQ_EINVAL, "null bytes");
-    *bytes = prefill_area_offset(L) + (M > DEC_MPAD ? pre_act_layout(L, M).bytes : 0);
+    size_t pre = 0;
+    if (M > DEC_MPAD) {
+        const int ks = prefill_ksplit(L, M);
+        pre = ((pre_act_layout(L, M).bytes + 255) & ~(size_t)255) + (ks > 1 ? (size_t)ks * M * L.N * 4 : 0);
+    }
+    *bytes = prefill_area_offset(L) + pre;
     return DYQ_OK;
 }
 

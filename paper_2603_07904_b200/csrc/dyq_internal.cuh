@@ -224,6 +224,9 @@ __device__ inline int warp_min_i(int v) { return __reduce_min_sync(0xffffffffu, 
 size_t decode_ws_bytes(const WLayout& L);
 dyq_status_t launch_prefetch_l2(const void* p, size_t bytes, cudaStream_t st);
 PreActLayout pre_act_layout(const WLayout& L, int M);
+// prefill split-K factor (1 = none) and the fp32 partial bytes it needs after
+// the prefill activation area
+int prefill_ksplit(const WLayout& L, int M);
 dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, const int32_t* row_bits, int bits,
                                  void* act, int64_t* err, cudaStream_t st, int gated = 0);
 dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,

@@ -87,6 +87,8 @@ struct PreArgs {
     int stages, stage_bytes;
     int off_meta, off_b, off_par, off_a;
     TpPeers tp;  // fused TP epilogue (TP instantiation only)
+    int ksplit;  // K-groups split over blockIdx.z (fp32 partials in `part`, summed by split_reduce_kernel)
+    float* part;
 };
 
 __device__ __forceinline__ int token_bits(const PreArgs& a, int m) { return a.row_bits ? a.row_bits[m] : a.bits; }
@@ -109,6 +111,10 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
     const WLayout& L = a.L;
     const int tile = blockIdx.x, tt = blockIdx.y;
     const int NG = L.NG;
+    // split-K: this CTA's groups [G0, G0 + NGL) (loop counters stay local so
+    // the stage / accumulator parities are unchanged)
+    const int G0 = (int)((blockIdx.z * (unsigned)NG) / a.ksplit);
+    const int NGL = (int)(((blockIdx.z + 1) * (unsigned)NG) / a.ksplit) - G0;
     const int S = a.stages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
@@ -183,16 +189,16 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             const uint32_t bbytes = f8 ? KSTEPS * BSTEP / 2 : KSTEPS * BSTEP;  // e4m3: K = 32 per step
             int s = 0;
             uint32_t ph = 0;
-            for (int g = 0; g < NG; ++g) {
+            for (int g = 0; g < NGL; ++g) {
                 if (g >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
                 // (DYQ_EXP_NO_* : timing experiments only, tools/build_variant.py)
                 constexpr int XM = DYQ_EXP_MASK;  // bit 0 codes, 1 meta, 2 B, 3 s_x skipped
                 ptx::mbar_arrive_expect_tx(&full[s], (XM & 1 ? 0 : cbytes) + (XM & 2 ? 0 : META_BLOCK) +
                                                          (XM & 4 ? 0 : bbytes) + (XM & 8 ? 0 : PAR_BYTES));
-                if (!(XM & 1)) ptx::bulk_g2s(st, a.codes + chunk_offset(L, tile, g * SPG, 0), cbytes, &full[s]);
-                if (!(XM & 2)) ptx::bulk_g2s(st + a.off_meta, a.meta + meta_block(L, tile, g), META_BLOCK, &full[s]);
-                const size_t tg = (size_t)tt * NG + g;
+                if (!(XM & 1)) ptx::bulk_g2s(st, a.codes + chunk_offset(L, tile, (G0 + g) * SPG, 0), cbytes, &full[s]);
+                if (!(XM & 2)) ptx::bulk_g2s(st + a.off_meta, a.meta + meta_block(L, tile, G0 + g), META_BLOCK, &full[s]);
+                const size_t tg = (size_t)tt * NG + G0 + g;
                 if (!(XM & 4)) ptx::bulk_g2s(st + a.off_b, a.act + a.P.x16_off + tg * a.P.x16_group, bbytes, &full[s]);
                 if (!(XM & 8)) ptx::bulk_g2s(st + a.off_par, a.act + a.P.par_off + tg * PAR_BYTES, PAR_BYTES, &full[s]);
                 tev(1, g);
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
         constexpr uint32_t idesc = tc::idesc_bf16(128, PT);
         int s = 0, ai = 0;
         uint32_t ph = 0, aph = 0;
-        for (int g = 0; g < NG; ++g) {
+        for (int g = 0; g < NGL; ++g) {
             const int b = g & 1;
             if (!(DYQ_EXP_MASK & 128)) {  // timing experiment: bit 7 = issue without waiting
             ptx::mbar_wait(&full[s], ph);      // B operand landed
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
         constexpr bool F8 = decltype(f8c)::value;
         int s = 0, ai = 0;
         uint32_t ph = 0, aph = 0;
-        for (int g = 0; g < NG; ++g) {
+        for (int g = 0; g < NGL; ++g) {
             ptx::mbar_wait(&full[s], ph);
             if (g >= NA) ptx::mbar_wait(&aempty[ai], aph ^ 1);
             tc::fence_after();
@@ -384,7 +390,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 #pragma unroll
         for (int c = 0; c < NB * 8; ++c) facc[c] = 0.f;
         int s = 0;
-        for (int g = 0; g < NG; ++g) {
+        for (int g = 0; g < NGL; ++g) {
             const int b = g & 1;
             ptx::mbar_wait(&tfull[b], (g >> 1) & 1);
             if (warp == PR_WARP0 && lane == 0) tev(6, g);
@@ -423,7 +429,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                             const int cl = h * NC + (blk0 + bi) * 8 + 2 * t + (j & 1), m = tt * PT + cl;
                             const int cf = s_col[cl];
                             if (cf != 0 && r < nsub * 16)
-                                a.I_out[((size_t)m * L.N + tile * 128 + r) * NG + g] =
+                                a.I_out[((size_t)m * L.N + tile * 128 + r) * NG + G0 + g] =
                                     cf == 2 ? 0 : __float2int_rn(__uint_as_float(v[si * 4 * nblk + bi * 4 + j]));
                         }
             };
@@ -466,7 +472,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             // memory ([column][row], row stride padded by 16 B against bank
             // conflicts), then write each token's row segment with 16-B stores.
             ptx::named_bar_sync(1, 256);  // all promotion warps are past their last stage read
-            const int es = a.y_dtype == 0 ? 4 : 2;
+            const int es = (a.ksplit > 1 || a.y_dtype == 0) ? 4 : 2;  // split-K partials are fp32
             const int rowp = 128 * es + 16;
 #pragma unroll
             for (int i = 0; i < NB * 8; ++i) {
@@ -492,8 +498,10 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                     for (int p = 0; p < a.tp.n; ++p)
                         *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.tp.y[p]) + o) = v;
                 } else {
-                    *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.y) + (m * L.N + tile * 128) * es + part * 16) =
-                        v;
+                    uint8_t* base = a.ksplit > 1
+                                        ? reinterpret_cast<uint8_t*>(a.part + (size_t)blockIdx.z * a.M * L.N)
+                                        : reinterpret_cast<uint8_t*>(a.y);
+                    *reinterpret_cast<uint4*>(base + (m * L.N + tile * 128) * es + part * 16) = v;
                 }
             }
             if constexpr (TP) {  // announce this CTA's nsub sub-tiles (see dec_tp_announce)
@@ -653,6 +661,57 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
     return check_launch("actquant_pre_kernel");
 }
 
+// y = sum_z part[z] in split order (deterministic), 4 outputs per thread.
+__global__ void split_reduce_kernel(const float* __restrict__ part, int ks, size_t MN, void* __restrict__ y,
+                                    int y_dtype) {
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i >= MN) return;
+    float4 acc = *reinterpret_cast<const float4*>(part + i);
+    for (int z = 1; z < ks; ++z) {
+        const float4 v = *reinterpret_cast<const float4*>(part + (size_t)z * MN + i);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (y_dtype == 0) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + i) = acc;
+    } else {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+        uint2 o;
+        o.x = *reinterpret_cast<uint32_t*>(&lo);
+        o.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(y) + i) = o;
+    }
+}
+
+static int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+            cudaGetLastError();
+            sms = 148;
+        }
+    }
+    return sms;
+}
+
+// Split the K-groups over up to 4 CTAs per output tile when the (tile, token
+// tile) grid fills less than half the SMs (o / down projections at M = 288:
+// 64 CTAs on 148 SMs), keeping >= 8 groups per split.  DYQ_PRE_KSPLIT=1
+// disables, =k forces at most k.
+int prefill_ksplit(const WLayout& L, int M) {
+    static const int cap = [] {
+        const char* v = getenv("DYQ_PRE_KSPLIT");
+        return v ? atoi(v) : 4;
+    }();
+    const int ctas = L.T128 * ((M + PT - 1) / PT);
+    int ks = 1;
+    while (ks < cap && ctas * (ks + 1) <= sm_count() && L.NG / (ks + 1) >= 8) ++ks;
+    return ks;
+}
+
 template <int WBITS, int SPG, bool PARTIALS, bool TP = false>
 static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
     PreArgs a = a0;
@@ -713,11 +772,30 @@ dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* met
     a.trace = g_trace;
     a.tp = {};
     if (tp) a.tp = *tp;
-    const dim3 grid(L.T128, (M + PT - 1) / PT);
+    a.ksplit = (I_out || tp || M <= DEC_MPAD) ? 1 : prefill_ksplit(L, M);  // workspace holds partials only for M > 16
+    a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(const_cast<void*>(act)) +
+                                      ((a.P.bytes + 255) & ~(size_t)255));
+    const dim3 grid(L.T128, (M + PT - 1) / PT, a.ksplit);
     const cudaError_t e = I_out ? pre_dispatch<true>(a, grid, st)
                           : tp  ? pre_dispatch<false, true>(a, grid, st)
                                 : pre_dispatch<false>(a, grid, st);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "qlinear_prefill_kernel launch: %s", cudaGetErrorString(e));
+    if (a.ksplit > 1) {
+        const size_t MN = (size_t)M * L.N;  // N % 16 == 0: whole float4 groups
+        const unsigned blocks = (unsigned)((MN / 4 + 255) / 256);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(blocks);
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cudaLaunchAttribute attr1[1];
+        attr1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr1[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = attr1;
+        cfg.numAttrs = 1;
+        const cudaError_t e2 = cudaLaunchKernelEx(&cfg, split_reduce_kernel, (const float*)a.part, a.ksplit, MN, y,
+                                                  y_dtype);
+        if (e2 != cudaSuccess) return set_error(DYQ_ECUDA, "split_reduce_kernel launch: %s", cudaGetErrorString(e2));
+    }
     return DYQ_OK;
 }
 
