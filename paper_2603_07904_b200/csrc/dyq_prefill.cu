@@ -697,19 +697,33 @@ static int sm_count() {
     return sms;
 }
 
-// Split the K-groups over up to 4 CTAs per output tile when the (tile, token
-// tile) grid fills less than half the SMs (o / down projections at M = 288:
-// 64 CTAs on 148 SMs), keeping >= 8 groups per split.  DYQ_PRE_KSPLIT=1
-// disables, =k forces at most k.
+// Split the K-groups over up to 4 CTAs per output tile when that shortens the
+// estimated wave schedule (o / down at M = 288: 64 CTAs on 148 SMs -> 2; qkv:
+// 192 CTAs -> 2; gate|up: 344 CTAs -> 1), keeping >= 8 groups per split.
+// DYQ_PRE_KSPLIT=k caps the split at k (1 disables).
 int prefill_ksplit(const WLayout& L, int M) {
     static const int cap = [] {
         const char* v = getenv("DYQ_PRE_KSPLIT");
         return v ? atoi(v) : 4;
     }();
-    const int ctas = L.T128 * ((M + PT - 1) / PT);
-    int ks = 1;
-    while (ks < cap && ctas * (ks + 1) <= sm_count() && L.NG / (ks + 1) >= 8) ++ks;
-    return ks;
+    static const int force = [] {
+        const char* v = getenv("DYQ_PRE_KSPLIT_FORCE");  // experiments (tools/): fixed split
+        return v ? atoi(v) : 0;
+    }();
+    if (force > 0) return (L.NG / force >= 1) ? force : 1;
+    // waves x per-CTA time, the latter ~ NG / ks + 20 group times of fixed
+    // cost (fitted to the M = 288 o / down / qkv / gate|up measurements)
+    const int ctas = L.T128 * ((M + PT - 1) / PT), sms = sm_count();
+    int best = 1;
+    double best_t = 1e30;
+    for (int ks = 1; ks <= cap && ks <= 4 && L.NG / ks >= 8; ++ks) {
+        const double t = (double)((ctas * ks + sms - 1) / sms) * ((double)L.NG / ks + 20.0);
+        if (t < best_t - 1e-9) {
+            best_t = t;
+            best = ks;
+        }
+    }
+    return best;
 }
 
 template <int WBITS, int SPG, bool PARTIALS, bool TP = false>
