@@ -61,6 +61,9 @@
 
 namespace dyq {
 
+#ifndef DYQ_AQP_THREADS
+#define DYQ_AQP_THREADS 256  // threads per prefill act-quant CTA (128 / 512: within 1 us per block)
+#endif
 constexpr int PT = 144;  // tokens per token tile (MMA N)
 static_assert(PT == PRE_PT, "dyq_tp_flag_delta counts prefill token tiles");
 constexpr int PRE_WARPS = 14;
@@ -647,8 +650,8 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
     const int TT = (M + PT - 1) / PT;
     const long long warps = (long long)TT * PT * L.NG;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)((warps * 32 + 255) / 256));
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3((unsigned)((warps * 32 + DYQ_AQP_THREADS - 1) / DYQ_AQP_THREADS));
+    cfg.blockDim = dim3(DYQ_AQP_THREADS);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
