@@ -61,6 +61,9 @@
 
 namespace dyq {
 
+#ifndef DYQ_PRE_MAX_STAGES
+#define DYQ_PRE_MAX_STAGES 8  // 4 / 6: same block time (316 us): the pipeline depth is not the bound
+#endif
 #ifndef DYQ_AQP_THREADS
 #define DYQ_AQP_THREADS 256  // threads per prefill act-quant CTA (128 / 512: within 1 us per block)
 #endif
@@ -741,7 +744,7 @@ static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
     a.off_a = 0;  // the A operand lives in TMEM
     a.stage_bytes = (a.off_par + PAR_BYTES + 127) & ~127;
     a.stages = (220 * 1024) / a.stage_bytes;
-    if (a.stages > 8) a.stages = 8;
+    if (a.stages > DYQ_PRE_MAX_STAGES) a.stages = DYQ_PRE_MAX_STAGES;
     if (a.stages < 2) a.stages = 2;
     const size_t smem = 1024 + (size_t)a.stages * a.stage_bytes;
     auto kern = qlinear_prefill_kernel<WBITS, SPG, PARTIALS, TP>;
