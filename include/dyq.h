@@ -137,7 +137,10 @@ DYQ_API dyq_status_t dyq_state_init(int32_t E, const dyq_calib_t* calib, void* s
                             dyq_stream_t stream);
 /* Episode reset for streams with mask[e] != 0 (mask: device u8 [E] or NULL =
  * all): clears windows, prev_rot, warm-up and the dispatcher; keeps the p95
- * history buffers (reading 23). */
+ * history buffers (reading 23).  The stream's next dyq_select_bits
+ * (or dyq_policy_step) does not observe its prev_action row: that action
+ * belongs to the previous episode (the decision at t uses the actions
+ * <= t-1 of the same episode), so the new episode starts like t = 0. */
 DYQ_API dyq_status_t dyq_state_reset_episode(void* state, const uint8_t* mask,
                                      dyq_stream_t stream);
 /* One control step for every stream: observe a_{t-1} (prev_action, device

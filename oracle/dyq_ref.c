@@ -214,6 +214,9 @@ typedef struct {
     int32_t Mwin_n, Mwin_pos, Jwin_n, Jwin_pos;
     double prev_rot[3];
     int32_t steps_seen; /* observations since (re)start; warm-up while < W_macro */
+    int32_t skip_next;  /* set by an episode reset: the next a_{t-1} is the previous
+                         * episode's last action and is not observed (reading 23;
+                         * the decision at t uses actions <= t-1 of THIS episode) */
     int32_t bstar, c, bbar; /* Alg. 1 state */
 } ref_stream_t;
 
@@ -228,6 +231,11 @@ static void stream_reset_episode(ref_stream_t* s) {
     s->prev_rot[0] = s->prev_rot[1] = s->prev_rot[2] = 0.0;
     s->steps_seen = 0;
     s->bstar = 16; s->c = 0; s->bbar = 16; /* S:254 safe cold start */
+}
+
+static void stream_new_episode(ref_stream_t* s) {
+    stream_reset_episode(s);
+    s->skip_next = 1;
 }
 
 void* dyq_ref_state_new(int32_t E, const dyq_ref_calib_t* cal) {
@@ -264,7 +272,7 @@ void dyq_ref_state_free(void* p) {
 void dyq_ref_state_reset_episode(void* p, const uint8_t* mask) {
     ref_state_t* st = (ref_state_t*)p;
     for (int32_t e = 0; e < st->E; ++e)
-        if (!mask || mask[e]) stream_reset_episode(&st->s[e]);
+        if (!mask || mask[e]) stream_new_episode(&st->s[e]);
 }
 
 static int cmp_double(const void* a, const void* b) {
@@ -367,7 +375,9 @@ int dyq_ref_select_bits(void* p, const float* prev_action, int32_t* bits,
     const dyq_ref_calib_t* c = &st->cal;
     for (int32_t e = 0; e < st->E; ++e) {
         ref_stream_t* s = &st->s[e];
-        if (prev_action) {
+        const int skip = s->skip_next;
+        s->skip_next = 0;
+        if (prev_action && !skip) {
             const float* a = prev_action + (int64_t)e * 7;
             const double x = a[0], y = a[1], z = a[2];
             const double r0 = a[3], r1 = a[4], r2 = a[5];

@@ -72,7 +72,9 @@ typedef struct {
 void* dyq_ref_state_new(int32_t E, const dyq_ref_calib_t* calib);
 void  dyq_ref_state_free(void* st);
 /* episode reset (reading 23): clears windows, prev_rot, warm-up counter and the
- * dispatcher (16,0,16); keeps the p95 history buffers.  mask may be NULL (all). */
+ * dispatcher (16,0,16); keeps the p95 history buffers; the stream's next
+ * select_bits does not observe its prev_action row (the previous episode's
+ * last action).  mask may be NULL (all). */
 void  dyq_ref_state_reset_episode(void* st, const uint8_t* mask);
 /* One control step for all E streams.  prev_action [E,7] = a_{t-1} (NULL at
  * t = 0: nothing observed).  Outputs (each may be NULL): bits [E] = b*_t,

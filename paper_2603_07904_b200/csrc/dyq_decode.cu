@@ -148,10 +148,25 @@ __device__ __forceinline__ float* dec_slot_scratch(const DecArgs& a, int sub) {
     return reinterpret_cast<float*>(smem + 256 + (size_t)a.stages * a.stage_bytes + 8 * 32 * 8 * 4) + sub * 256;
 }
 // Lane 0 of a contributor warp: once its bulk slot store completed, count it.
+// The slot was written by the async proxy and is read by the reducer through
+// the generic proxy after its ld.acquire of the counter: the increment is a
+// gpu-scope RELEASE preceded by an async->generic proxy fence (PTX memory
+// model; DYQ_DEC_RELAXED_PUBLISH=1 restores the relaxed increment for A/B).
+#ifndef DYQ_DEC_RELAXED_PUBLISH
+#define DYQ_DEC_RELAXED_PUBLISH 0
+#endif
+__device__ __forceinline__ void dec_count_slot(int* p) {
+#if DYQ_DEC_RELAXED_PUBLISH
+    ptx::red_add_relaxed_gpu(p, 1);
+#else
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    ptx::red_add_release_gpu(p, 1);
+#endif
+}
 __device__ __forceinline__ void dec_publish(int*& pend, int lane) {
     if (lane == 0 && pend) {
         ptx::bulk_wait_all();
-        ptx::red_add_relaxed_gpu(pend, 1);
+        dec_count_slot(pend);
         pend = nullptr;
     }
 }
@@ -211,7 +226,7 @@ __device__ __forceinline__ void dec_flush_warp(const DecArgs& a, int tile, const
         __syncwarp();
         if (lane == 0) {
             ptx::bulk_wait_all();  // previous publication of this warp (scratch reuse)
-            if (pend) ptx::red_add_relaxed_gpu(pend, 1);
+            if (pend) dec_count_slot(pend);
             float* P = a.part + ((size_t)(base + c) * 8 + sub) * 16 * 16;
             ptx::bulk_s2g(P, ptx::smem_u32(scr), NT8 * 8 * 16 * 4);
             pend = cnt;

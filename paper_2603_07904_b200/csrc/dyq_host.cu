@@ -234,9 +234,11 @@ dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* byt
     if (rc) return rc;
     if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range [0, 65536]");
     if (!bytes) return set_error(DYQ_EINVAL, "null bytes");
+    // the prefill activation area is reserved for every M > 0: dyq_set_path(2)
+    // routes even M <= 16 through the prefill kernels (split-K only for M > 16)
     size_t pre = 0;
-    if (M > DEC_MPAD) {
-        const int ks = prefill_ksplit(L, M);
+    if (M > 0) {
+        const int ks = M > DEC_MPAD ? prefill_ksplit(L, M) : 1;
         pre = ((pre_act_layout(L, M).bytes + 255) & ~(size_t)255) + (ks > 1 ? (size_t)ks * M * L.N * 4 : 0);
     }
     *bytes = prefill_area_offset(L) + pre;

@@ -796,13 +796,17 @@ static dyq_status_t model_layout(const dyq_model_desc_t* m, ModelLayout* L) {
     const size_t MP = L->MP, d = m->d, ffn = m->ffn;
     for (int which = 0; which < 4; ++which) {
         const dyq_wdesc_t w = wdesc_of(*m, which);
+        // a step may run any e <= desc.E episodes (prefill M = e * S, decode
+        // M = e) and the prefill split factor is not monotone in M, so the
+        // workspace is the maximum over every M the step can issue
         size_t wsb = 0;
-        for (int M : {L->MP, m->E}) {
-            size_t b = 0;
-            dyq_status_t rc = dyq_qlinear_workspace(&w, M, &b);
-            if (rc) return rc;
-            wsb = b > wsb ? b : wsb;
-        }
+        for (int e = 1; e <= m->E; ++e)
+            for (int M : {e * L->S, e}) {
+                size_t b = 0;
+                dyq_status_t rc = dyq_qlinear_workspace(&w, M, &b);
+                if (rc) return rc;
+                wsb = b > wsb ? b : wsb;
+            }
         L->ws_bytes[which] = wsb;
     }
     size_t o = 0;

@@ -32,7 +32,9 @@ struct SelHeader {
 constexpr size_t SEL_HDR = 256;
 static_assert(sizeof(SelHeader) <= SEL_HDR, "header");
 
-enum { I_HIST_N = 0, I_HIST_POS, I_MW_N, I_MW_POS, I_JW_N, I_JW_POS, I_STEPS, I_BSTAR, I_C, I_BBAR, I_COUNT };
+// I_SKIP: set by an episode reset -- the stream's next a_{t-1} belongs to the
+// previous episode and is not observed (reading 23, S:259 causality)
+enum { I_HIST_N = 0, I_HIST_POS, I_MW_N, I_MW_POS, I_JW_N, I_JW_POS, I_STEPS, I_BSTAR, I_C, I_BBAR, I_SKIP, I_COUNT };
 
 __host__ inline SelHeader make_sel_header(int32_t E, const dyq_calib_t& c) {
     SelHeader h{};
@@ -79,13 +81,16 @@ __global__ void sel_init_kernel(uint8_t* state) {
     int32_t* I = reinterpret_cast<int32_t*>(base + h.off_int);
     I[I_HIST_N] = I[I_HIST_POS] = 0;
     reset_episode_dev(h, base);
+    I[I_SKIP] = 0;
 }
 
 __global__ void sel_reset_kernel(uint8_t* state, const uint8_t* mask) {
     const SelHeader h = *reinterpret_cast<const SelHeader*>(state);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < h.E; e += gridDim.x * blockDim.x) {
         if (mask && !mask[e]) continue;
-        reset_episode_dev(h, state + SEL_HDR + (size_t)e * h.stride);
+        uint8_t* base = state + SEL_HDR + (size_t)e * h.stride;
+        reset_episode_dev(h, base);
+        reinterpret_cast<int32_t*>(base + h.off_int)[I_SKIP] = 1;
     }
 }
 
@@ -164,6 +169,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_bits_kernel(uint8_t* state
     }
     __syncthreads();
     const SelHeader& h = *reinterpret_cast<const SelHeader*>(ssm);
+    if (e >= h.E) return;  // block-uniform: more CTAs than initialised streams
     const dyq_calib_t& c = h.cal;
     uint8_t* gbase = state + SEL_HDR + (size_t)e * h.stride;
     uint8_t* base = ssm + SEL_HDR;
@@ -179,7 +185,10 @@ __global__ void __launch_bounds__(SEL_THREADS) select_bits_kernel(uint8_t* state
     int32_t* I = reinterpret_cast<int32_t*>(base + h.off_int);
     __syncthreads();
 
-    if (observe) {
+    const bool skip = I[I_SKIP] != 0;  // first step after an episode reset: a_{t-1} is stale
+    __syncthreads();
+    if (skip && threadIdx.x == 0) I[I_SKIP] = 0;
+    if (observe && !skip) {
         if (threadIdx.x == 0) {
             const double x = act[0], y = act[1], z = act[2];
             const double r0 = act[3], r1 = act[4], r2 = act[5];

@@ -153,3 +153,58 @@ def test_act_quant_a16_rows_pass_through():
     assert np.all(aq.xq[1] == 0) and np.all(aq.s[1] == 0)
     assert aq.xq[0].max() <= 255 and aq.xq[2].max() <= 3
     assert np.array_equal(aq.SX, aq.xq.reshape(3, 2, 64).astype(np.int32).sum(-1))
+
+
+# ---------------------------------------------------------------- round_mode=1
+# DESIGN.md reading 1: Eq. (2) prints a floor; round_mode = 1 is the
+# nearest-integer option, floor(v / s + 1/2).  Pins: hand-computed halves on an
+# exactly representable grid, the exact rational definition, and the fixed-grid
+# round trip that holds for nearest rounding but not for floor.
+
+def test_nearest_mode_hand_cases():
+    # s = 0.25 (exact), z = 4, 4 bits: v / s = 2, 2.5, 1.5, -0.5, -1.5, 9.999.., 100
+    v = [0.5, 0.625, 0.375, -0.125, -0.375, 2.4999, 25.0]
+    assert oracle.quantize(v, 0.25, 4, 4, round_mode=1).tolist() == [6, 7, 6, 4, 3, 14, 15]
+    assert oracle.quantize(v, 0.25, 4, 4, round_mode=0).tolist() == [6, 6, 5, 3, 2, 13, 15]
+
+
+def test_nearest_mode_is_exact_rational_rounding():
+    rng = np.random.default_rng(17)
+    for _ in range(200):
+        s = float(np.float32(abs(rng.standard_normal()) * 0.05 + 1e-3))
+        z = int(rng.integers(0, 16))
+        v = (rng.standard_normal(64) * 0.3).astype(np.float32).astype(np.float64)
+        # include exact half-way points (k + 1/2) * s where representable
+        v[:8] = [float(np.float32((k + 0.5) * s)) for k in range(-4, 4)]
+        q = oracle.quantize(v, s, z, 4, round_mode=1)
+        for vi, qi in zip(v, q):
+            r = Fraction(vi) / Fraction(s) + Fraction(1, 2)
+            want = min(max(int(r.__floor__()) + z, 0), 15)
+            assert qi == want
+
+
+def test_nearest_mode_fixed_grid_round_trip():
+    """q(s (q - z)) == q on the fixed grid with an fp32 x-hat in nearest mode;
+    floor mode misses it for a large share of codes (App. A item 6)."""
+    rng = np.random.default_rng(23)
+    miss_floor = 0
+    for _ in range(300):
+        v = (rng.standard_normal(64) * 0.2).astype(np.float32).astype(np.float64)
+        s, z = oracle.quant_fit(v, 4)
+        q = oracle.quantize(v, s, z, 4, round_mode=1)
+        xh32 = oracle.dequantize(q, s, z).astype(np.float32).astype(np.float64)
+        assert np.array_equal(oracle.quantize(xh32, s, z, 4, round_mode=1), q)
+        miss_floor += int(np.any(oracle.quantize(xh32, s, z, 4, round_mode=0) != q))
+    assert miss_floor > 30
+
+
+def test_nearest_mode_reconstruction_bound():
+    """Nearest rounding halves the S:81 bound: |x - xhat| <= s / 2 (+ fp32
+    rounding of xhat) for every x inside the zero-inclusive range."""
+    rng = np.random.default_rng(29)
+    for bits in (2, 4, 8):
+        for _ in range(200):
+            v = (rng.standard_normal(64) * rng.uniform(0.01, 3)).astype(np.float32).astype(np.float64)
+            s, z = oracle.quant_fit(v, bits)
+            xh = oracle.dequantize(oracle.quantize(v, s, z, bits, round_mode=1), s, z)
+            assert np.all(np.abs(v - xh) <= 0.5 * s * (1 + 2 ** -20) + 1e-30)

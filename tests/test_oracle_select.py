@@ -187,3 +187,64 @@ def test_bits_mix_with_history():
     bits = r["bits"][120:]
     vals = set(np.unique(bits).tolist())
     assert vals == {2, 4, 8, 16}
+
+
+def test_reset_episode_hand_trace():
+    """DESIGN.md reading 23: an episode reset clears the windows,
+    the previous rotation, the warm-up count and Alg. 1 (-> (16, 0, 16)) but
+    KEEPS the p95 history rings; the first step after it does not observe its
+    a_{t-1} (the previous episode's last action).  Hand trace with exact
+    binary fractions: 20 steps of ||xyz|| = 1 (mu = 1) and rotation jumps of
+    0.25 (nu = 0.25), reset, then ||xyz|| = 0.5:
+      step 0 after the reset: nothing observed -> empty windows, S = 0, 16;
+      first observation: M = 1 - 0.5 / 1 = 0.5 (a wiped ring would give
+      mu = 0.5, M = 0), jerk = 0 (prev_rot cleared), Mbar = 0.5 (windows
+      cleared), S = 0.25, warm-up -> 16;
+      second: rot jumps 0.25 -> J = 0.25 / 0.25 = 1, Jbar = (0 + 1) / 2,
+      S = 0.5 * 0.5 + 0.5 * 0.5 = 0.5."""
+    st = oracle.SelectState(1)
+    a = np.zeros((1, 7), np.float32)
+    a[0, 0] = 1.0
+    st.step(None)
+    for i in range(20):
+        a[0, 3] = 0.25 * (i % 2)
+        r = st.step(a)
+    assert r["bits"][0] in (2, 4, 8, 16) and r["target"][0] != 16  # out of warm-up before the reset
+    st.reset_episode()
+    r0 = st.step(a)  # a is the previous episode's last action: not observed
+    assert r0["Mbar"][0] == 0.0 and r0["Jbar"][0] == 0.0 and r0["S"][0] == 0.0
+    assert r0["target"][0] == 16 and r0["bits"][0] == 16
+    b = np.zeros((1, 7), np.float32)
+    b[0, 0] = 0.5
+    b[0, 3] = 0.125
+    r1 = st.step(b)
+    assert r1["Mbar"][0] == 0.5 and r1["Jbar"][0] == 0.0 and r1["S"][0] == 0.25
+    assert r1["target"][0] == 16 and r1["bits"][0] == 16
+    b[0, 3] = 0.375
+    r2 = st.step(b)
+    assert r2["Mbar"][0] == 0.5 and r2["Jbar"][0] == 0.5 and r2["S"][0] == 0.5
+    assert r2["bits"][0] == 16
+    # warm-up restarts: W_macro = 10 observations after the reset; then, with
+    # the rotation held (J = 0, Jbar = 0 once obs 2 leaves the 5-window),
+    # S = 0.25 -> 4 bits (Theta = (0.1, 0.3)), entered by Alg. 1 from
+    # (16, 0, 16) after K = 3 consecutive targets
+    outs = [st.step(b) for _ in range(12)]  # observations 3 .. 14
+    tg = [int(o["target"][0]) for o in outs]
+    bits = [int(o["bits"][0]) for o in outs]
+    assert [float(o["S"][0]) for o in outs[4:]] == [0.25] * 8
+    assert tg[:7] == [16] * 7 and tg[7:] == [4] * 5  # obs 10 = first after warm-up
+    assert bits[:9] == [16] * 9 and bits[9:] == [4] * 3
+
+
+def test_reset_episode_mask_leaves_other_streams():
+    acts = synth.trajectories(3, 60)
+    st = oracle.SelectState(3)
+    ref = oracle.replay(acts)
+    for t in range(60):
+        if t == 30:
+            st.reset_episode(np.array([0, 1, 0], np.uint8))
+        r = st.step(None if t == 0 else acts[t - 1])
+        assert r["bits"][0] == ref["bits"][t, 0] and r["bits"][2] == ref["bits"][t, 2]
+        assert r["S"][0] == ref["S"][t, 0] and r["S"][2] == ref["S"][t, 2]
+        if t == 30:  # stream 1 starts over: nothing observed, warm-up
+            assert r["bits"][1] == 16 and r["target"][1] == 16 and r["S"][1] == 0.0
