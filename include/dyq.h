@@ -179,6 +179,14 @@ DYQ_API dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t toke
 DYQ_API dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* bytes);
 DYQ_API dyq_status_t dyq_workspace_init(void* workspace, size_t bytes, dyq_stream_t stream);
 
+/* The launch plan dyq_qlinear / dyq_qlinear_i32_partials use for M rows of
+ * this shape (host only, no device work): *path = 1 decode kernel (M <= 16),
+ * 2 tcgen05 prefill kernel; *ksplit = K-group split factor of the prefill
+ * grid (1 = none; > 1: each split writes fp32 partial tiles reduced in split
+ * order, or its own groups of the integer partials).  Either pointer may be
+ * NULL.  Lets tests assert which code path a parity case exercised. */
+DYQ_API dyq_status_t dyq_qlinear_plan(const dyq_wdesc_t* wd, int32_t M, int32_t* path, int32_t* ksplit);
+
 /* ------------------------------------------------------------- qlinear */
 /* y[m,n] = Sum_g s_x[m,g] s_w[n,g] Sum_{k in g} (Xq[m,k]-z_x[m,g]) (q[n,k]-z_w[n,g])
  * for integer rows (row_bits[m] in {2,4,8}); the codes Xq are the dynamic

@@ -12,15 +12,15 @@
 //    metadata (one copy) + the activation records of those K-groups (one copy,
 //    plus one for the bf16 rows of BF16-bypass tokens) -- big copies keep the
 //    TMA engine's per-copy cost off the critical path;
-//  * stream-K: contiguous unit ranges, tile-major, one CTA per SM; 8 consumer
-//    warps (warp w = 16-row sub-tile w) + 1 producer warp, <= 113 KB of shared
-//    memory and <= 112 registers per thread so that TWO CTAs fit on an SM: under
-//    programmatic dependent launch (PDL) the next layer's CTAs become resident
-//    while this layer drains and stream their weights into their own ring
-//    (issued before griddepcontrol.wait -- weights never depend on the previous
-//    kernel), hiding the per-call dependency latency (act-quant -> MMA);
-//  * consumer math per (sub-tile, group): one LDS.128 per lane is the
-//    exact register image of two mma.m16n8k32 A fragments (pre-permuted by
+//  * stream-K: contiguous unit ranges, tile-major, ONE CTA per SM (544
+//    threads: 16 consumer warps + 1 producer warp, up to 56 KB of codes per
+//    stage).  Under programmatic dependent launch (PDL) the producer issues
+//    its first stages' weight copies BEFORE griddepcontrol.wait -- weights
+//    never depend on the previous kernel -- so weight streaming overlaps the
+//    tail of the preceding kernel (act-quant or the previous linear);
+//  * consumer warp w owns 16-row sub-tile w & 7 and the even / odd groups
+//    (w >> 3) of every stage; one LDS.128 per lane is the exact register
+//    image of two mma.m16n8k32 A fragments (pre-permuted by
 //    dyq_pack_weights); nibbles widen with LOP3s; integer tokens run
 //    IMMA.16832.U8.U8 (tokens = the n8 dimension) with the exact per-group
 //    zero-point algebra
@@ -28,11 +28,15 @@
 //    where Sum q comes from one more IMMA against an all-ones B (no shuffles);
 //    A2/A4-only calls use centred s8 codes (I = P' - z_w*SXc, one IMMA);
 //    A16 tokens (the BF16 bypass) convert the same registers to bf16
-//    (q - z_w is exact) and run HMMA.16816 against x;
-//  * y = Sum_g s_x s_w I in fp32 (packed FMUL2/FFMA2); a tile split across
-//    CTAs is reduced per WARP (no CTA barrier): each contributor writes a
-//    private slot, the last to arrive on the (tile, sub-tile) counter sums the
-//    slots in contributor order (deterministic) and writes y.
+//    (q - z_w is exact) and run HMMA.16816 against x; the two parity warps of
+//    a sub-tile combine through shared memory (64-thread named barrier);
+//  * y = Sum_g s_x s_w I in fp32 (packed FMUL2/FFMA2).  A tile split across
+//    CTAs is reduced by a DESIGNATED reducer: the contributors of a tile are
+//    CTAs c_first..c_last, c_first holds the tile's first groups at the END of
+//    its range, so it reduces; the others publish a private slot (smem ->
+//    cp.async.bulk -> completion wait -> counter increment) and never wait;
+//    c_first acquires the counter, sums the slots in contributor order
+//    (deterministic) and writes y.
 #include <stdlib.h>
 
 #include "dyq_internal.cuh"
@@ -148,12 +152,17 @@ __device__ __forceinline__ float* dec_slot_scratch(const DecArgs& a, int sub) {
     return reinterpret_cast<float*>(smem + 256 + (size_t)a.stages * a.stage_bytes + 8 * 32 * 8 * 4) + sub * 256;
 }
 // Lane 0 of a contributor warp: once its bulk slot store completed, count it.
-// The slot was written by the async proxy and is read by the reducer through
-// the generic proxy after its ld.acquire of the counter: the increment is a
-// gpu-scope RELEASE preceded by an async->generic proxy fence (PTX memory
-// model; DYQ_DEC_RELAXED_PUBLISH=1 restores the relaxed increment for A/B).
+// The slot was written by the async proxy (cp.async.bulk shared->global) and
+// is read by the reducer through the generic proxy after its ld.acquire of
+// the counter.  The writer has already waited for the bulk store to COMPLETE
+// (cp.async.bulk.wait_group 0, i.e. the bytes are in L2, the gpu-scope
+// coherence point) before it increments, so a relaxed increment is ordered
+// after the data on this hardware; the PTX-model-strict form (async->generic
+// proxy fence + red.release.gpu) costs ~1.2 us per gate|up call (B200 A/B:
+// 12.65 -> 13.9 us, 35a9e9e) and is kept as a build switch
+// (DYQ_DEC_RELAXED_PUBLISH=0).  DESIGN.md §5 records the trade.
 #ifndef DYQ_DEC_RELAXED_PUBLISH
-#define DYQ_DEC_RELAXED_PUBLISH 0
+#define DYQ_DEC_RELAXED_PUBLISH 1
 #endif
 __device__ __forceinline__ void dec_count_slot(int* p) {
 #if DYQ_DEC_RELAXED_PUBLISH

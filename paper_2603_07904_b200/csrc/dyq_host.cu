@@ -245,6 +245,17 @@ dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* byt
     return DYQ_OK;
 }
 
+dyq_status_t dyq_qlinear_plan(const dyq_wdesc_t* wd, int32_t M, int32_t* path, int32_t* ksplit) {
+    WLayout L;
+    dyq_status_t rc = validate_wdesc(wd, &L);
+    if (rc) return rc;
+    if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range [0, 65536]");
+    const bool pre = g_path == 2 || (g_path == 0 && M > DEC_MPAD);
+    if (path) *path = pre ? 2 : 1;
+    if (ksplit) *ksplit = (pre && M > DEC_MPAD) ? prefill_ksplit(L, M) : 1;
+    return DYQ_OK;
+}
+
 dyq_status_t dyq_workspace_init(void* ws, size_t bytes, dyq_stream_t stream) {
     if (!ws && bytes) return set_error(DYQ_EINVAL, "null workspace");
     if (bytes && cudaMemsetAsync(ws, 0, bytes, (cudaStream_t)stream) != cudaSuccess)

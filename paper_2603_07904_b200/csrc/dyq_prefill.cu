@@ -792,7 +792,10 @@ dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* met
     a.trace = g_trace;
     a.tp = {};
     if (tp) a.tp = *tp;
-    a.ksplit = (I_out || tp || M <= DEC_MPAD) ? 1 : prefill_ksplit(L, M);  // workspace holds partials only for M > 16
+    // split-K applies to the integer partials too (each split writes its own
+    // groups of I_out, so the split path is bit-checked); the fp32 partial
+    // tiles live in the workspace, reserved only for M > 16
+    a.ksplit = (tp || M <= DEC_MPAD) ? 1 : prefill_ksplit(L, M);
     a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(const_cast<void*>(act)) +
                                       ((a.P.bytes + 255) & ~(size_t)255));
     const dim3 grid(L.T128, (M + PT - 1) / PT, a.ksplit);
@@ -800,7 +803,7 @@ dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* met
                           : tp  ? pre_dispatch<false, true>(a, grid, st)
                                 : pre_dispatch<false>(a, grid, st);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "qlinear_prefill_kernel launch: %s", cudaGetErrorString(e));
-    if (a.ksplit > 1) {
+    if (a.ksplit > 1 && !I_out) {
         const size_t MN = (size_t)M * L.N;  // N % 16 == 0: whole float4 groups
         const unsigned blocks = (unsigned)((MN / 4 + 255) / 256);
         cudaLaunchConfig_t cfg = {};

@@ -33,6 +33,7 @@ _SIGS = {
     "dyq_route_bits": [P, i32, i32, P, P, P],
     "dyq_select_route": [P, i32, P, P, i32, P, P, P, P, P],
     "dyq_qlinear_workspace": [P, i32, P],
+    "dyq_qlinear_plan": [P, i32, P, P],
     "dyq_workspace_init": [P, sz, P],
     "dyq_qlinear": [P, P, P, P, i32, P, i32, P, i32, P, sz, P, P],
     "dyq_qlinear_i32_partials": [P, P, P, P, i32, P, i32, P, P, sz, P, P],
@@ -239,6 +240,13 @@ def route_bits(bits, E: int, tokens_per_episode: int, row_bits, abits_of=None, s
 
 
 # ---------------------------------------------------------------- qlinear
+def qlinear_plan(wd: WDesc, M: int) -> tuple[int, int]:
+    """(path, ksplit) of a qlinear call with M rows: path 1 decode, 2 prefill."""
+    p, k = C.c_int32(0), C.c_int32(0)
+    _call("dyq_qlinear_plan", C.byref(wd), M, C.byref(p), C.byref(k))
+    return p.value, k.value
+
+
 def qlinear_workspace(wd: WDesc, M: int) -> int:
     b = C.c_size_t(0)
     _call("dyq_qlinear_workspace", C.byref(wd), M, C.byref(b))

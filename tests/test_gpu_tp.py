@@ -4,6 +4,7 @@ column split composed on one GPU against the unsharded qlinear."""
 import numpy as np
 import pytest
 
+import oracle
 import synth
 
 pytestmark = pytest.mark.gpu
@@ -13,6 +14,7 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from paper_2603_07904_b200 import dyq  # noqa: E402
+from test_gpu_parity import check_close  # noqa: E402
 
 DEV = "cuda:0"
 
@@ -53,3 +55,7 @@ def test_two_shard_composition(M):
     y_tp = torch.cat(parts, dim=1)
     # same codes and integer sums; fp32 split-K order may differ per tile assignment
     torch.testing.assert_close(y_tp, y_full, rtol=1e-5, atol=1e-5 * float(y_full.abs().max()))
+    # and the joined shards are the oracle qlinear of the UNSHARDED weight
+    w_h, x_h = W.cpu().numpy().view(np.uint16), x.cpu().numpy().view(np.uint16)
+    yref, _ = oracle.qlinear(x_h, oracle.pack_weights(w_h, 64, 4), 64, 4)
+    check_close(y_tp.cpu().numpy(), yref, 1e-3)

@@ -9,6 +9,7 @@ import socket
 import numpy as np
 import pytest
 
+import oracle
 import synth
 
 pytestmark = pytest.mark.gpu
@@ -18,6 +19,7 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from paper_2603_07904_b200 import dyq  # noqa: E402
+from test_gpu_parity import check_close  # noqa: E402
 
 DEV = "cuda:0"
 
@@ -39,6 +41,10 @@ def test_fused_simulated_ranks(P, M, N):
     rb = torch.tensor([[2, 4, 8, 16][m % 4] for m in range(M)], dtype=torch.int32, device=DEV)
     delta = dyq.tp_flag_delta(N, M)
     assert delta == N // 16 * (1 if M <= 16 else -(-M // 144))
+    # oracle reference: the UNSHARDED weight's qlinear (a K-group never spans
+    # ranks, so the gathered column shards must be exactly its columns)
+    w_h, x_h = W.cpu().numpy().view(np.uint16), x.cpu().numpy().view(np.uint16)
+    pk_full = oracle.pack_weights(w_h, 64, 4)
     for c, (bits, row_bits) in enumerate([(4, None), (2, None), (0, rb), (16, None)], start=1):
         s = (c - 1) % 2
         for r in range(P):
@@ -53,6 +59,8 @@ def test_fused_simulated_ranks(P, M, N):
                         dim=1).view(torch.int16)
         for r in range(P):
             assert torch.equal(ys[s][r], ref), (c, r)
+        yref, _ = oracle.qlinear(x_h, pk_full, 64, bits if row_bits is None else row_bits.cpu().numpy())
+        check_close(ys[s][0].view(torch.bfloat16).float().cpu().numpy(), yref, 2e-2)
 
 
 def test_fused_rejects_bad_peers_and_forced_decode_over_16():
