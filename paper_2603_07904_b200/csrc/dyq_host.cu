@@ -224,8 +224,10 @@ dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t tpe, const i
 // Workspace = [decode split-K accumulator + tile counters (must start zeroed;
 // self-cleaning)] [standalone activation-quantizer output (dyq_act_quant)].
 static size_t act_area_offset(const WLayout& L) { return (decode_ws_bytes(L) + 255) & ~(size_t)255; }
+// The 1 KB before the prefill area holds the prefill stream-K unit counters
+// (fixed position per shape, so they stay zeroed for every M; self-resetting).
 static size_t prefill_area_offset(const WLayout& L) {
-    return (act_area_offset(L) + act_layout_dec(L, 2).bytes + 1023) & ~(size_t)1023;
+    return ((act_area_offset(L) + act_layout_dec(L, 2).bytes + 1023) & ~(size_t)1023) + PRE_CNT_BYTES;
 }
 
 dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* bytes) {
@@ -237,10 +239,7 @@ dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* byt
     // the prefill activation area is reserved for every M > 0: dyq_set_path(2)
     // routes even M <= 16 through the prefill kernels (split-K only for M > 16)
     size_t pre = 0;
-    if (M > 0) {
-        const int ks = M > DEC_MPAD ? prefill_ksplit(L, M) : 1;
-        pre = ((pre_act_layout(L, M).bytes + 255) & ~(size_t)255) + (ks > 1 ? (size_t)ks * M * L.N * 4 : 0);
-    }
+    if (M > 0) pre = ((pre_act_layout(L, M).bytes + 255) & ~(size_t)255) + prefill_part_bytes(L, M);
     *bytes = prefill_area_offset(L) + pre;
     return DYQ_OK;
 }
@@ -252,7 +251,7 @@ dyq_status_t dyq_qlinear_plan(const dyq_wdesc_t* wd, int32_t M, int32_t* path, i
     if (M < 0 || M > 65536) return set_error(DYQ_ESHAPE, "M out of range [0, 65536]");
     const bool pre = g_path == 2 || (g_path == 0 && M > DEC_MPAD);
     if (path) *path = pre ? 2 : 1;
-    if (ksplit) *ksplit = (pre && M > DEC_MPAD) ? prefill_ksplit(L, M) : 1;
+    if (ksplit) *ksplit = pre ? prefill_ksplit(L, M) : 1;
     return DYQ_OK;
 }
 

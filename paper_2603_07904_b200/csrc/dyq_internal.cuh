@@ -117,9 +117,11 @@ __device__ __forceinline__ bool dec_call_centred(int M, int m0, const int32_t* r
 //   x16 [TT][NG][G/16 K-steps][144 rows] bf16: centred codes Xq - z_x (exact),
 //       x for A16 rows, 0 for absent rows
 //   par [TT][NG][144] f32 s_x (1 for A16 rows, 0 for absent rows)
+//   mode [TT] u8: 1 = the tile's operands are e4m3 (dyq_pre_tile_e4m3)
 // (codes_off / codes_group are unused, kept 0).
+constexpr size_t PRE_CNT_BYTES = 1024;  // prefill stream-K counters, just before the prefill area
 struct PreActLayout {
-    size_t codes_off, x16_off, par_off, bytes;
+    size_t codes_off, x16_off, par_off, mode_off, bytes;
     size_t codes_group, x16_group;
 };
 
@@ -224,9 +226,11 @@ __device__ inline int warp_min_i(int v) { return __reduce_min_sync(0xffffffffu, 
 size_t decode_ws_bytes(const WLayout& L);
 dyq_status_t launch_prefetch_l2(const void* p, size_t bytes, cudaStream_t st);
 PreActLayout pre_act_layout(const WLayout& L, int M);
-// prefill split-K factor (1 = none) and the fp32 partial bytes it needs after
-// the prefill activation area
+// prefill stream-K: the largest number of CTAs sharing one output tile (1 =
+// none split) and the fp32 partial-tile bytes the workspace reserves after the
+// prefill activation area
 int prefill_ksplit(const WLayout& L, int M);
+size_t prefill_part_bytes(const WLayout& L, int M);
 dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, const int32_t* row_bits, int bits,
                                  void* act, int64_t* err, cudaStream_t st, int gated = 0);
 dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,

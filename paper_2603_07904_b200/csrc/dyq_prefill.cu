@@ -51,35 +51,32 @@
 #include "dyq_internal.cuh"
 #include "dyq_ptx.cuh"
 
-// timing-only build switches (tools/build_variant.py), 0 in product builds
-#ifndef DYQ_EXP_MASK
-#define DYQ_EXP_MASK 0
-#endif
-#ifndef DYQ_PREFILL_TRACE
-#define DYQ_PREFILL_TRACE 0
-#endif
 
 namespace dyq {
 
 #ifndef DYQ_PRE_MAX_STAGES
 #define DYQ_PRE_MAX_STAGES 8  // 4 / 6: same block time (316 us): the pipeline depth is not the bound
 #endif
-#ifndef DYQ_AQP_THREADS
-#define DYQ_AQP_THREADS 256  // threads per prefill act-quant CTA (128 / 512: within 1 us per block)
-#endif
 constexpr int PT = 144;  // tokens per token tile (MMA N)
 static_assert(PT == PRE_PT, "dyq_tp_flag_delta counts prefill token tiles");
-constexpr int PRE_WARPS = 14;
+// warps: 0 weight producer, 1 MMA issuer, 2 activation producer, 3-6
+// transform, 7-14 promotion.  A warp may only touch TMEM lanes of quadrant
+// (warp id % 4): the transform warps cover quadrants 3, 0, 1, 2 and each
+// column half of the promotion warps covers all four.  (Registers: each SM
+// sub-partition holds 16 K, so > 12 warps per CTA cap a thread at 128.)
+constexpr int PRE_WARPS = 15;
 constexpr int PRE_THREADS = PRE_WARPS * 32;
 constexpr int PAR_BYTES = PT * 4;  // per (tile, group): float s_x[144] (1 for A16 tokens, 0 for absent)
-constexpr int XF_WARPS = 4;
-constexpr int PR_WARP0 = 2 + XF_WARPS;  // first promotion warp
+constexpr int XF_WARP0 = 3, XF_WARPS = 4;
+constexpr int PR_WARP0 = 7, PR_WARPS = 8;  // promotion warps
+constexpr int STG_ROW = 128 * 2 + 16;  // epilogue staging: bytes per token (128 bf16 rows + pad)
+#ifndef DYQ_PRE_MIN_GROUPS
+#define DYQ_PRE_MIN_GROUPS 16  // stream-K: at least this many K-groups per CTA
+#endif
 constexpr uint32_t ACC_COLS = 2 * PT;   // TMEM: two 144-column accumulators, then the A buffers
 
 struct PreArgs {
     WLayout L;
-    int e4m3;  // e4m3 mode allowed (W4; DYQ_PRE_E4M3=1 enables)
-    uint64_t* trace;  // dyq_trace_enable buffer: per-group events of CTA (0,0), or null
     const uint8_t* codes;
     const uint8_t* meta;
     const int32_t* row_bits;
@@ -88,16 +85,22 @@ struct PreArgs {
     void* y;
     int y_dtype;
     int32_t* I_out;
-    const uint8_t* act;  // prefill activation area
+    const uint8_t* act;  // prefill activation area (B operand, s_x, per-tile mode bytes)
     PreActLayout P;
     int stages, stage_bytes;
-    int off_meta, off_b, off_par, off_a;
-    TpPeers tp;  // fused TP epilogue (TP instantiation only)
-    int ksplit;  // K-groups split over blockIdx.z (fp32 partials in `part`, summed by split_reduce_kernel)
-    float* part;
+    int off_meta, off_b, off_par;
+    int off_stage;       // epilogue staging area (bytes from the dynamic smem base)
+    int TT;              // 144-token tiles
+    long long W;         // work groups = T128 * TT * NG, split contiguously over gridDim.x CTAs
+    TpPeers tp;          // fused TP epilogue (TP instantiation only; one whole unit per CTA)
+    float* part;         // stream-K partial tiles [2 * gridDim.x][144 tokens][128 rows] fp32
+    int* cnt;            // [gridDim.x] per-reducer arrival counters (zeroed once, self-resetting)
+    uint64_t* trace;     // dyq_trace_enable buffer or null (kernel id 2; events below)
+    uint32_t serial;
 };
-
-__device__ __forceinline__ int token_bits(const PreArgs& a, int m) { return a.row_bits ? a.row_bits[m] : a.bits; }
+// trace events (tools/trace_prefill.py): 0 CTA entry, 1 promotion past
+// griddepcontrol.wait, 2 first accumulator ready, 3 segment's last group
+// promoted, 4 segment epilogue done (reducer: after its wait), 5 CTA exit
 
 // Physical byte position, inside one 32-k e4m3 K step, of logical k (0..31):
 // the packed W4 fragment puts k = 4t + i (low nibbles) in TMEM column 2t and
@@ -107,6 +110,11 @@ __device__ __forceinline__ uint8_t e4m3_of(float v) {  // exact for integers |v|
     return (uint8_t)__nv_cvt_float_to_fp8(v, __NV_SATFINITE, __NV_E4M3);
 }
 
+// Stream-K partition: CTA c owns work groups [sk_begin(c), sk_begin(c + 1)) of
+// the flat order w = ((tile * TT + tt) * NG + g) -- tile-major, so the token
+// tiles of one weight tile run back to back (its codes stay in L2).
+__host__ __device__ inline long long sk_begin(long long W, int P, int c) { return (W * c) / P; }
+
 template <int WBITS, int SPG, bool PARTIALS, bool TP>
 __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const PreArgs a) {
     constexpr int G = SPG * 64;
@@ -115,17 +123,15 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
     constexpr int NA = SPG == 1 ? 6 : 3;   // A-operand buffers in TMEM
     constexpr uint32_t A_COLS = 8 * KSTEPS;
     const WLayout& L = a.L;
-    const int tile = blockIdx.x, tt = blockIdx.y;
-    const int NG = L.NG;
-    // split-K: this CTA's groups [G0, G0 + NGL) (loop counters stay local so
-    // the stage / accumulator parities are unchanged)
-    const int G0 = (int)((blockIdx.z * (unsigned)NG) / a.ksplit);
-    const int NGL = (int)(((blockIdx.z + 1) * (unsigned)NG) / a.ksplit) - G0;
+    const int NG = L.NG, TT = a.TT;
+    const long long w0 = sk_begin(a.W, gridDim.x, blockIdx.x), w1 = sk_begin(a.W, gridDim.x, blockIdx.x + 1);
+    const int nw = (int)(w1 - w0);
     const int S = a.stages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
+    const uint8_t* mode = a.act + a.P.mode_off;  // per token tile: 1 = e4m3 operands (written by the quantizer)
 
     extern __shared__ __align__(1024) uint8_t smem[];
+    if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 2, 0);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;   // [2]
@@ -133,44 +139,16 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
     uint64_t* afull = tempty + 2;  // [NA]
     uint64_t* aempty = afull + NA; // [NA]
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(aempty + NA);
-    uint8_t* s_col = smem + 512;  // per token column: 0 absent, 1 integer bits, 2 BF16 bypass
-    // per-group event ev of CTA (0,0): a plain store at trace[16 + 512 ev + g]
-    // (no atomics: tracing adds no latency to the pipeline it observes)
-    // (compiled in only with -DDYQ_PREFILL_TRACE=1, tools/build_variant.py:
-    // even untaken, the checks cost the hot loops ~5 %)
-#if DYQ_PREFILL_TRACE
-    uint64_t* const tr = (blockIdx.x == 0 && blockIdx.y == 0) ? a.trace : nullptr;
-    auto tev = [&](uint32_t ev, int g) {
-        if (tr && g < 512) {
-            uint64_t t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            tr[16 + 512 * ev + g] = t;
-        }
-    };
-#else
-    auto tev = [](uint32_t, int) {};
-#endif
     uint8_t* stage0 = smem + 1024;
 
-    ptx::pdl_wait();  // the B operand, s_x and row_bits come from the preceding kernels
-    if (threadIdx.x == 0) ptx::pdl_launch_dependents();
-    int ok8 = 1;
-    for (int i = threadIdx.x; i < PT; i += PRE_THREADS) {
-        const int m = tt * PT + i;
-        const int bm = m < a.M ? token_bits(a, m) : 2;
-        s_col[i] = m < a.M ? (bm == 16 ? 2 : 1) : 0;
-        ok8 &= (bm == 2 || bm == 4);
-    }
-    // tile mode (uniform per CTA; the quantizer decides identically)
-    const bool f8 = WBITS == 4 && a.e4m3 && __syncthreads_and(ok8);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], 1 + 8 + XF_WARPS);  // MMA commit + promotion + transform warps
+            ptx::mbar_init(&full[s], 2);  // weight producer + activation producer
+            ptx::mbar_init(&empty[s], 1 + XF_WARPS + PR_WARPS);  // MMA commit + transform + promotion warps
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&tfull[b], 1);
-            ptx::mbar_init(&tempty[b], 8);
+            ptx::mbar_init(&tempty[b], PR_WARPS);
         }
         for (int i = 0; i < NA; ++i) {
             ptx::mbar_init(&afull[i], XF_WARPS);
@@ -187,52 +165,82 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
     tc::fence_after();
     const uint32_t tmem = *s_tmem;
     const uint32_t sbase = ptx::smem_u32(stage0);
+    // walk of this CTA's groups: (unit u = tile * TT + tt, group g)
+    struct Walk {
+        int tile, tt, g;
+    };
+    auto walk0 = [&]() {
+        const int u = (int)(w0 / NG);
+        return Walk{u / TT, u % TT, (int)(w0 - (long long)u * NG)};
+    };
+    auto next = [&](Walk& k) {
+        if (++k.g == NG) {
+            k.g = 0;
+            if (++k.tt == TT) {
+                k.tt = 0;
+                ++k.tile;
+            }
+        }
+    };
 
     if (warp == 0) {
-        // ------------------------------------------------------ producer
+        // ------------------------------------------------ weight producer
+        // Weights never depend on the preceding kernel: the first stages are
+        // issued before griddepcontrol.wait, overlapping its tail under PDL.
         if (lane == 0) {
-            const uint32_t cbytes = (uint32_t)(SPG * nsub * L.chunk);
-            const uint32_t bbytes = f8 ? KSTEPS * BSTEP / 2 : KSTEPS * BSTEP;  // e4m3: K = 32 per step
+            Walk k = walk0();
             int s = 0;
             uint32_t ph = 0;
-            for (int g = 0; g < NGL; ++g) {
-                if (g >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
+            for (int i = 0; i < nw; ++i, next(k)) {
+                if (i >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
+                const int nsub = (k.tile == L.T128 - 1) ? L.nsub_last : 8;
+                const uint32_t cbytes = (uint32_t)(SPG * nsub * L.chunk);
                 uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
-                // (DYQ_EXP_NO_* : timing experiments only, tools/build_variant.py)
-                constexpr int XM = DYQ_EXP_MASK;  // bit 0 codes, 1 meta, 2 B, 3 s_x skipped
-                ptx::mbar_arrive_expect_tx(&full[s], (XM & 1 ? 0 : cbytes) + (XM & 2 ? 0 : META_BLOCK) +
-                                                         (XM & 4 ? 0 : bbytes) + (XM & 8 ? 0 : PAR_BYTES));
-                if (!(XM & 1)) ptx::bulk_g2s(st, a.codes + chunk_offset(L, tile, (G0 + g) * SPG, 0), cbytes, &full[s]);
-                if (!(XM & 2)) ptx::bulk_g2s(st + a.off_meta, a.meta + meta_block(L, tile, G0 + g), META_BLOCK, &full[s]);
-                const size_t tg = (size_t)tt * NG + G0 + g;
-                if (!(XM & 4)) ptx::bulk_g2s(st + a.off_b, a.act + a.P.x16_off + tg * a.P.x16_group, bbytes, &full[s]);
-                if (!(XM & 8)) ptx::bulk_g2s(st + a.off_par, a.act + a.P.par_off + tg * PAR_BYTES, PAR_BYTES, &full[s]);
-                tev(1, g);
+                ptx::mbar_arrive_expect_tx(&full[s], cbytes + META_BLOCK);
+                ptx::bulk_g2s(st, a.codes + chunk_offset(L, k.tile, k.g * SPG, 0), cbytes, &full[s]);
+                ptx::bulk_g2s(st + a.off_meta, a.meta + meta_block(L, k.tile, k.g), META_BLOCK, &full[s]);
+                if (++s == S) { s = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 2) {
+        // -------------------------------------------- activation producer
+        ptx::pdl_wait();  // the B operand, s_x and the mode bytes come from the quantizer
+        if (lane == 0) ptx::pdl_launch_dependents();
+        if (lane == 0) {
+            Walk k = walk0();
+            int s = 0;
+            uint32_t ph = 0;
+            for (int i = 0; i < nw; ++i, next(k)) {
+                if (i >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
+                const uint32_t bbytes = mode[k.tt] ? KSTEPS * BSTEP / 2 : KSTEPS * BSTEP;  // e4m3: K = 32 per step
+                uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
+                const size_t tg = (size_t)k.tt * NG + k.g;
+                ptx::mbar_arrive_expect_tx(&full[s], bbytes + PAR_BYTES);
+                ptx::bulk_g2s(st + a.off_b, a.act + a.P.x16_off + tg * a.P.x16_group, bbytes, &full[s]);
+                ptx::bulk_g2s(st + a.off_par, a.act + a.P.par_off + tg * PAR_BYTES, PAR_BYTES, &full[s]);
                 if (++s == S) { s = 0; ph ^= 1; }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer
+        ptx::pdl_wait();
         constexpr uint32_t idesc = tc::idesc_bf16(128, PT);
+        constexpr uint32_t idesc8 = tc::idesc_e4m3(128, PT);
+        Walk k = walk0();
         int s = 0, ai = 0;
         uint32_t ph = 0, aph = 0;
-        for (int g = 0; g < NGL; ++g) {
-            const int b = g & 1;
-            if (!(DYQ_EXP_MASK & 128)) {  // timing experiment: bit 7 = issue without waiting
+        for (int i = 0; i < nw; ++i, next(k)) {
+            const int b = i & 1;
+            const bool f8 = WBITS == 4 && mode[k.tt];
             ptx::mbar_wait(&full[s], ph);      // B operand landed
-            if (lane == 0) tev(2, g);
             ptx::mbar_wait(&afull[ai], aph);   // A operand written to TMEM
-            if (lane == 0) tev(3, g);
-            if (g >= 2) ptx::mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
-            if (lane == 0) tev(4, g);
-            }
+            if (i >= 2) ptx::mbar_wait(&tempty[b], ((i >> 1) - 1) & 1);
             tc::fence_after();
             if (lane == 0) {
                 const uint32_t st = sbase + s * a.stage_bytes;
                 const uint32_t d = tmem + b * PT;
                 const uint32_t at = tmem + ACC_COLS + ai * A_COLS;
                 if (f8) {
-                    constexpr uint32_t idesc8 = tc::idesc_e4m3(128, PT);
 #pragma unroll
                     for (int ks = 0; ks < KSTEPS / 2; ++ks) {
                         const uint64_t bd = tc::smem_desc(st + a.off_b + ks * BSTEP, 128, 256);
@@ -253,22 +261,23 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             if (++s == S) { s = 0; ph ^= 1; }
             if (++ai == NA) { ai = 0; aph ^= 1; }
         }
-    } else if (warp < PR_WARP0) {
+    } else if (warp >= XF_WARP0 && warp < XF_WARP0 + XF_WARPS) {
         // ------------------------------------------------------ transform
         // Warp with TMEM quadrant q writes the A rows of sub-tiles 2q and 2q+1
         // (TMEM lanes 32q.. and 32q+16..).  Lane (gid, t) owns lane-chunk
         // (gid, t) of each sub-tile: rows gid and gid+8, k = 4t..4t+3 of every K
         // step -- exactly the 16x256b register fragment, so each sub-tile and
         // slab pair is one LDS.128 and one tcgen05.st.16x256b.x4.
+        ptx::pdl_wait();
         const int q = warp & 3;
-        // one loop per tile mode (the mode is uniform per CTA): no per-group branch
-        auto transform = [&](auto f8c) {
-        constexpr bool F8 = decltype(f8c)::value;
+        Walk k = walk0();
         int s = 0, ai = 0;
         uint32_t ph = 0, aph = 0;
-        for (int g = 0; g < NGL; ++g) {
+        for (int i = 0; i < nw; ++i, next(k)) {
+            const bool f8 = WBITS == 4 && mode[k.tt];
+            const int nsub = (k.tile == L.T128 - 1) ? L.nsub_last : 8;
             ptx::mbar_wait(&full[s], ph);
-            if (g >= NA) ptx::mbar_wait(&aempty[ai], aph ^ 1);
+            if (i >= NA) ptx::mbar_wait(&aempty[ai], aph ^ 1);
             tc::fence_after();
             const uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
             const uint8_t* zrow = st + a.off_meta + 512;
@@ -276,11 +285,11 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 #pragma unroll
             for (int si = 0; si < 2; ++si) {
                 const int sub = 2 * q + si;
-                if (sub >= nsub || (DYQ_EXP_MASK & 64)) break;
+                if (sub >= nsub) break;
                 const uint32_t tl = at + ((uint32_t)(32 * q + 16 * si) << 16);
                 // zero points of rows gid and gid+8 are adjacent metadata slots
                 const uint32_t z01 = *reinterpret_cast<const uint16_t*>(zrow + sub * 16 + 2 * (lane >> 2));
-                if constexpr (WBITS == 4 && F8) {
+                if (WBITS == 4 && f8) {
                     // e4m3 (q - z_w): K step = slab; TMEM column 2t <- low nibbles,
                     // 2t + 1 <- high nibbles (e4m3_kpos), rows gid / gid + 8
                     const float zf0 = 8388608.f + (float)(z01 & 0xffu), zf1 = 8388608.f + (float)(z01 >> 8);
@@ -300,7 +309,6 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 #pragma unroll
                                 for (int bb = 0; bb < 4; ++bb)  // (2^23 + q) - (2^23 + z): exact q - z
                                     v[bb] = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7540u + bb)) - zf;
-                                // two cvt.rn.satfinite.e4m3x2.f32 (low byte = first value)
                                 const uint32_t p01 = __nv_cvt_float2_to_fp8x2(make_float2(v[0], v[1]), __NV_SATFINITE, __NV_E4M3);
                                 const uint32_t p23 = __nv_cvt_float2_to_fp8x2(make_float2(v[2], v[3]), __NV_SATFINITE, __NV_E4M3);
                                 r[slab * 4 + rs * 2 + hn] = (p01 & 0xffffu) | (p23 << 16);
@@ -372,155 +380,217 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             if (lane == 0) {
                 ptx::mbar_arrive(&afull[ai]);
                 ptx::mbar_arrive(&empty[s]);
-                if (warp == 2) tev(5, g);
             }
             if (++s == S) { s = 0; ph ^= 1; }
             if (++ai == NA) { ai = 0; aph ^= 1; }
         }
-        };
-        if (f8)
-            transform(std::true_type{});
-        else
-            transform(std::false_type{});
-    } else {
+    } else if (warp >= PR_WARP0) {
         // ------------------------------------------------------ promotion
         // 16x256b loads: thread (gid, t) holds rows 32q + 16 si + gid (+8) and
         // columns 8 blk + 2t, 2t+1 -- each thread needs only 18 of the 72 s_x.
+        // Outer loop: this CTA's segments (one unit each); inner loop: the
+        // segment's K-groups; the epilogue runs once per segment.
+        ptx::pdl_wait();
+        const bool tr0 = a.trace && threadIdx.x == PR_WARP0 * 32;
+        if (tr0) trace_ev(a.trace, a.serial, 2, 1);
         const int e = warp - PR_WARP0;  // 0..7
         const int q = warp & 3;         // TMEM lane quadrant (hardware: warp id % 4)
         const int h = e >> 2;           // column half: tokens [72h, 72h + 72)
         const int gid = lane >> 2, t = lane & 3;
         constexpr int NC = PT / 2;      // 72 columns per warp
         constexpr int NB = NC / 8;      // 9 column blocks
+        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + h * NC;
+        const int swo = (2 * q) * 16 + 2 * gid;  // s_w slot of rows gid / gid + 8 of sub-tile 2q (+16: 2q+1)
+        const int sxo = h * NC + 2 * t;          // first s_x of this thread
         float facc[NB * 8];             // [blk][si][j]
 #pragma unroll
         for (int c = 0; c < NB * 8; ++c) facc[c] = 0.f;
-        int s = 0;
-        for (int g = 0; g < NGL; ++g) {
-            const int b = g & 1;
-            ptx::mbar_wait(&tfull[b], (g >> 1) & 1);
-            if (warp == PR_WARP0 && lane == 0) tev(6, g);
-            tc::fence_after();
-            const uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
-            const float* swp = reinterpret_cast<const float*>(st + a.off_meta);
-            const float2 sw0 = *reinterpret_cast<const float2*>(swp + (2 * q) * 16 + 2 * gid);      // sub 2q
-            const float2 sw1 = *reinterpret_cast<const float2*>(swp + (2 * q + 1) * 16 + 2 * gid);  // sub 2q+1
-            const float* sxp = reinterpret_cast<const float*>(st + a.off_par) + h * NC + 2 * t;
-            const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + b * PT + h * NC;
-            auto promote = [&](const uint32_t* v, int nblk, int blk0) {
+        int s = 0, i = 0;
+        long long w = w0;
+        while (w < w1) {
+            const int u = (int)(w / NG);
+            const int g0 = (int)(w - (long long)u * NG);
+            const int g1 = (w1 - (long long)u * NG) < NG ? (int)(w1 - (long long)u * NG) : NG;  // exclusive
+            const int tile = u / TT, tt = u - tile * TT;
+            const int nsub = (tile == L.T128 - 1) ? L.nsub_last : 8;
+            for (int g = g0; g < g1; ++g, ++i) {
+                const int b = i & 1;
+                ptx::mbar_wait(&tfull[b], (i >> 1) & 1);
+                if (tr0 && i == 0) trace_ev(a.trace, a.serial, 2, 2);
+                tc::fence_after();
+                const uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
+                const float* swp = reinterpret_cast<const float*>(st + a.off_meta) + swo;
+                const float2 sw0 = *reinterpret_cast<const float2*>(swp);       // sub 2q
+                const float2 sw1 = *reinterpret_cast<const float2*>(swp + 16);  // sub 2q+1
+                const float* sxp = reinterpret_cast<const float*>(st + a.off_par) + sxo;
+                const uint32_t tb = tq + b * PT;
+                auto promote = [&](const uint32_t* v, int nblk, int blk0) {
 #pragma unroll
-                for (int bi = 0; bi < nblk; ++bi) {
-                    const float2 sx = *reinterpret_cast<const float2*>(sxp + (blk0 + bi) * 8);
+                    for (int bi = 0; bi < nblk; ++bi) {
+                        const float2 sx = *reinterpret_cast<const float2*>(sxp + (blk0 + bi) * 8);
 #pragma unroll
-                    for (int si = 0; si < 2; ++si) {
-                        const uint32_t* vv = v + si * 4 * nblk + bi * 4;
-                        const float2 sw = si ? sw1 : sw0;
-                        float* fa = facc + ((blk0 + bi) * 2 + si) * 4;
-                        float t0, t1, t2, t3;
-                        ptx::mul2f(t0, t1, __uint_as_float(vv[0]), __uint_as_float(vv[1]), sx.x, sx.y);
-                        ptx::mul2f(t2, t3, __uint_as_float(vv[2]), __uint_as_float(vv[3]), sx.x, sx.y);
-                        ptx::fma2f(fa[0], fa[1], t0, t1, sw.x, sw.x);
-                        ptx::fma2f(fa[2], fa[3], t2, t3, sw.y, sw.y);
-                    }
-                }
-            };
-            auto partials = [&](const uint32_t* v, int nblk, int blk0) {
-#pragma unroll
-                for (int bi = 0; bi < nblk; ++bi)
-#pragma unroll
-                    for (int si = 0; si < 2; ++si)
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int r = 32 * q + 16 * si + gid + 8 * (j >> 1);
-                            const int cl = h * NC + (blk0 + bi) * 8 + 2 * t + (j & 1), m = tt * PT + cl;
-                            const int cf = s_col[cl];
-                            if (cf != 0 && r < nsub * 16)
-                                a.I_out[((size_t)m * L.N + tile * 128 + r) * NG + G0 + g] =
-                                    cf == 2 ? 0 : __float2int_rn(__uint_as_float(v[si * 4 * nblk + bi * 4 + j]));
+                        for (int si = 0; si < 2; ++si) {
+                            const uint32_t* vv = v + si * 4 * nblk + bi * 4;
+                            const float2 sw = si ? sw1 : sw0;
+                            float* fa = facc + ((blk0 + bi) * 2 + si) * 4;
+                            float t0, t1, t2, t3;
+                            ptx::mul2f(t0, t1, __uint_as_float(vv[0]), __uint_as_float(vv[1]), sx.x, sx.y);
+                            ptx::mul2f(t2, t3, __uint_as_float(vv[2]), __uint_as_float(vv[3]), sx.x, sx.y);
+                            ptx::fma2f(fa[0], fa[1], t0, t1, sw.x, sw.x);
+                            ptx::fma2f(fa[2], fa[3], t2, t3, sw.y, sw.y);
                         }
-            };
-            constexpr int XM2 = DYQ_EXP_MASK;  // timing experiments: bit 4 no promotion math, bit 5 no TMEM loads
-            if (XM2 & 32) {
-                tc::fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[b]);
-            } else {
+                    }
+                };
+                auto partials = [&](const uint32_t* v, int nblk, int blk0) {
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {  // blocks 0-3, 4-7
-                uint32_t v[32];
-                tc::ld16x256_x4(tb + c * 32, v);
-                tc::ld16x256_x4(tb + (16u << 16) + c * 32, v + 16);
-                tc::wait_ld();
-                if (PARTIALS) partials(v, 4, c * 4);
-                else if (!(XM2 & 16)) promote(v, 4, c * 4);
-                else facc[c] += __uint_as_float(v[c]);
-            }
-            {  // block 8
-                uint32_t v[8];
-                tc::ld16x256_x1(tb + 64, v);
-                tc::ld16x256_x1(tb + (16u << 16) + 64, v + 4);
-                tc::wait_ld();
-                tc::fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[b]);
-                if (PARTIALS) partials(v, 1, 8);
-                else if (!(XM2 & 16)) promote(v, 1, 8);
-                else facc[2] += __uint_as_float(v[2]);
-            }
-            }
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&empty[s]);
-            if (warp == PR_WARP0 && lane == 0) tev(7, g);
-            if (++s == S) s = 0;
-        }
-        if constexpr (!PARTIALS) {
-            // Epilogue: transpose the 128 x 144 tile through (now idle) stage
-            // memory ([column][row], row stride padded by 16 B against bank
-            // conflicts), then write each token's row segment with 16-B stores.
-            ptx::named_bar_sync(1, 256);  // all promotion warps are past their last stage read
-            const int es = (a.ksplit > 1 || a.y_dtype == 0) ? 4 : 2;  // split-K partials are fp32
-            const int rowp = 128 * es + 16;
+                    for (int bi = 0; bi < nblk; ++bi)
 #pragma unroll
-            for (int i = 0; i < NB * 8; ++i) {
-                const int blk = i >> 3, si = (i >> 2) & 1, j = i & 3;
-                const int r = 32 * q + 16 * si + gid + 8 * (j >> 1);
-                const int c = h * NC + blk * 8 + 2 * t + (j & 1);
-                uint8_t* o = stage0 + c * rowp + r * es;
-                if (es == 4)
-                    *reinterpret_cast<float*>(o) = facc[i];
-                else
-                    *reinterpret_cast<__nv_bfloat16*>(o) = __float2bfloat16_rn(facc[i]);
+                        for (int si = 0; si < 2; ++si)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const int r = 32 * q + 16 * si + gid + 8 * (j >> 1);
+                                const int m = tt * PT + sxo + (blk0 + bi) * 8 + (j & 1);
+                                if (m < a.M && r < nsub * 16) {
+                                    const int bm = a.row_bits ? a.row_bits[m] : a.bits;
+                                    a.I_out[((size_t)m * L.N + tile * 128 + r) * NG + g] =
+                                        bm == 16 ? 0 : __float2int_rn(__uint_as_float(v[si * 4 * nblk + bi * 4 + j]));
+                                }
+                            }
+                };
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {  // blocks 0-3, 4-7
+                    uint32_t v[32];
+                    tc::ld16x256_x4(tb + c * 32, v);
+                    tc::ld16x256_x4(tb + (16u << 16) + c * 32, v + 16);
+                    tc::wait_ld();
+                    if (PARTIALS) partials(v, 4, c * 4);
+                    else promote(v, 4, c * 4);
+                }
+                {  // block 8
+                    uint32_t v[8];
+                    tc::ld16x256_x1(tb + 64, v);
+                    tc::ld16x256_x1(tb + (16u << 16) + 64, v + 4);
+                    tc::wait_ld();
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[b]);
+                    if (PARTIALS) partials(v, 1, 8);
+                    else promote(v, 1, 8);
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&empty[s]);
+                if (++s == S) s = 0;
             }
-            ptx::named_bar_sync(1, 256);
-            const int cpc = 128 * es / 16;  // 16-B chunks per token column
-            const int valid = nsub * 16 * es / 16;
-            for (int k = threadIdx.x - PR_WARP0 * 32; k < PT * cpc; k += 256) {
-                const int c = k / cpc, part = k - c * cpc;
-                if (part >= valid || s_col[c] == 0) continue;
-                const size_t m = (size_t)tt * PT + c;
-                const uint4 v = *reinterpret_cast<const uint4*>(stage0 + c * rowp + part * 16);
-                if constexpr (TP) {  // bf16 into every rank's full y, this rank's columns
-                    const size_t o = (m * a.tp.ldy + a.tp.col0 + tile * 128) * 2 + part * 16;
-                    for (int p = 0; p < a.tp.n; ++p)
-                        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.tp.y[p]) + o) = v;
+            if (tr0) trace_ev(a.trace, a.serial, 2, 3);
+            if constexpr (!PARTIALS) {
+                // ---- segment end.  whole unit: y directly; otherwise an fp32
+                // partial tile [144 tokens][128 rows] for prefill_fixup_kernel
+                // (slot 2c: the CTA's first segment started mid-unit, else 2c+1)
+                const bool whole = g0 == 0 && g1 == NG;
+                const int rb = 32 * q + gid;  // row of element (si 0, j 0)
+                const int mb = tt * PT + sxo;  // token of element (blk 0, j 0)
+                // y for one finished tile: bf16 outputs are transposed through
+                // the staging area ([token][row], 272-B rows) and leave as
+                // coalesced 16-B stores of each token's 128-row segment;
+                // fp32 outputs (tests) are stored directly.
+                auto write_out = [&]() {
+                    if (!TP && a.y_dtype == 0) {
+                        const size_t n0 = (size_t)tile * 128 + rb;
+#pragma unroll
+                        for (int ii = 0; ii < NB * 8; ++ii) {
+                            const int blk = ii >> 3, si = (ii >> 2) & 1, j = ii & 3;
+                            const int dr = 16 * si + 8 * (j >> 1), dm = blk * 8 + (j & 1);
+                            if (rb + dr < nsub * 16 && mb + dm < a.M)
+                                reinterpret_cast<float*>(a.y)[(size_t)(mb + dm) * L.N + n0 + dr] = facc[ii];
+                            facc[ii] = 0.f;
+                        }
+                        return;
+                    }
+                    uint8_t* stg = smem + a.off_stage;
+#pragma unroll
+                    for (int ii = 0; ii < NB * 8; ++ii) {
+                        const int blk = ii >> 3, si = (ii >> 2) & 1, j = ii & 3;
+                        *reinterpret_cast<__nv_bfloat16*>(stg + (sxo + blk * 8 + (j & 1)) * STG_ROW +
+                                                          (rb + 16 * si + 8 * (j >> 1)) * 2) =
+                            __float2bfloat16_rn(facc[ii]);
+                        facc[ii] = 0.f;
+                    }
+                    ptx::named_bar_sync(1, PR_WARPS * 32);
+                    const int tid = threadIdx.x - PR_WARP0 * 32;
+                    for (int k = tid; k < PT * 16; k += PR_WARPS * 32) {
+                        const int c = k >> 4, part = k & 15;
+                        const int m = tt * PT + c;
+                        if (part >= 2 * nsub || m >= a.M) continue;
+                        const uint4 v = *reinterpret_cast<const uint4*>(stg + c * STG_ROW + part * 16);
+                        if constexpr (TP) {  // bf16 into every rank's full y, this rank's columns
+                            const size_t o = ((size_t)m * a.tp.ldy + a.tp.col0 + (size_t)tile * 128) * 2 + part * 16;
+                            for (int p = 0; p < a.tp.n; ++p)
+                                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.tp.y[p]) + o) = v;
+                        } else {
+                            *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.y) +
+                                                      ((size_t)m * L.N + (size_t)tile * 128) * 2 + part * 16) = v;
+                        }
+                    }
+                    ptx::named_bar_sync(1, PR_WARPS * 32);  // staging free for the next tile
+                };
+                if (whole) {
+                    write_out();
+                    if constexpr (TP) {  // announce this unit's nsub sub-tiles (see dec_tp_announce)
+                        if (threadIdx.x == PR_WARP0 * 32) {
+                            __threadfence_system();
+                            for (int p = 0; p < a.tp.n; ++p) atomicAdd_system(a.tp.flag[p], (unsigned long long)nsub);
+                        }
+                    }
+                } else if (g0 != 0) {
+                    // HEAD part of a unit split across CTAs (this CTA's first
+                    // segment): an fp32 partial tile [144 tokens][128 rows] in
+                    // slot c, then one arrival on the reducer's counter.  The
+                    // reducer is the CTA holding the unit's first groups, which
+                    // reaches them at the END of its range, so it rarely waits.
+                    float* slot = a.part + (size_t)blockIdx.x * (PT * 128) + sxo * 128 + rb;
+#pragma unroll
+                    for (int ii = 0; ii < NB * 8; ++ii) {
+                        const int blk = ii >> 3, si = (ii >> 2) & 1, j = ii & 3;
+                        __stcg(slot + (blk * 8 + (j & 1)) * 128 + 16 * si + 8 * (j >> 1), facc[ii]);
+                        facc[ii] = 0.f;
+                    }
+                    ptx::named_bar_sync(1, PR_WARPS * 32);
+                    if (threadIdx.x == PR_WARP0 * 32) {
+                        const long long ub = (long long)u * NG;
+                        const int c_lo = (int)(((ub + 1) * gridDim.x - 1) / a.W);  // CTA holding group ub
+                        __threadfence();
+                        atomicAdd(a.cnt + c_lo, 1);
+                    }
                 } else {
-                    uint8_t* base = a.ksplit > 1
-                                        ? reinterpret_cast<uint8_t*>(a.part + (size_t)blockIdx.z * a.M * L.N)
-                                        : reinterpret_cast<uint8_t*>(a.y);
-                    *reinterpret_cast<uint4*>(base + (m * L.N + tile * 128) * es + part * 16) = v;
+                    // REDUCER: this CTA holds the unit's first groups (its last
+                    // segment); the other contributors c + 1 .. c_hi each
+                    // published a head slot.  Sum in CTA order (deterministic).
+                    const long long ue = (long long)(u + 1) * NG;
+                    const int c_hi = (int)((ue * gridDim.x - 1) / a.W);  // CTA holding group ue - 1
+                    if (threadIdx.x == PR_WARP0 * 32) {
+                        const int need = c_hi - (int)blockIdx.x;
+                        while (ptx::ld_acquire_gpu(a.cnt + blockIdx.x) < need) __nanosleep(64);
+                        a.cnt[blockIdx.x] = 0;  // self-reset (no other arrival targets this CTA this call)
+                    }
+                    ptx::named_bar_sync(1, PR_WARPS * 32);
+                    for (int cc = (int)blockIdx.x + 1; cc <= c_hi; ++cc) {
+                        const float* slot = a.part + (size_t)cc * (PT * 128) + sxo * 128 + rb;
+#pragma unroll
+                        for (int ii = 0; ii < NB * 8; ++ii) {
+                            const int blk = ii >> 3, si = (ii >> 2) & 1, j = ii & 3;
+                            facc[ii] += __ldcg(slot + (blk * 8 + (j & 1)) * 128 + 16 * si + 8 * (j >> 1));
+                        }
+                    }
+                    write_out();
                 }
             }
-            if constexpr (TP) {  // announce this CTA's nsub sub-tiles (see dec_tp_announce)
-                ptx::named_bar_sync(1, 256);
-                if (threadIdx.x == PR_WARP0 * 32) {
-                    __threadfence_system();
-                    for (int p = 0; p < a.tp.n; ++p) atomicAdd_system(a.tp.flag[p], (unsigned long long)nsub);
-                }
-            }
+            if (tr0) trace_ev(a.trace, a.serial, 2, 4);
+            w += g1 - g0;
         }
     }
     tc::fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 2, 5);
     if (warp == 1) {
         tc::fence_after();
         tc::dealloc(tmem, 512);
@@ -528,100 +598,132 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 }
 
 // -------------------------------------------- prefill activation quantizer
-// One warp per (token tile tt, token row 0..143, group g).  Writes the B operand
-// in the UMMA canonical K-major bf16 layout
-//   [tt][g][K step ks][row>>3][kk>>3][row&7][kk&7]   (16 k per K step)
+// One CTA per (token tile tt, K-group g); thread pair (2 row, 2 row + 1) of
+// the 288 threads quantizes token row `row` of the tile: each thread holds 32
+// of the group's G = 64 inputs (16-B loads), the pair combines min / max with
+// one shuffle, and each thread writes its K steps of the B operand in the
+// UMMA canonical K-major layout with 16-B stores
+//   bf16: [tt][g][K step ks][row>>3][kk>>3][row&7][kk&7]   (16 k per K step)
+//   e4m3: [tt][g][K step ks][row>>3][p>>4][row&7][p&15]    (32 k per K step,
+//         p = e4m3_kpos(k))
 // holding the centred codes Xq - z_x of Eq. (2) for integer tokens (exact in
-// bf16), x itself for A16 tokens and 0 for absent rows; and s_x per token
-// (1 for A16 tokens, 0 for absent rows).
-__global__ void actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
-                                    const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ act,
-                                    PreActLayout P, int64_t* err, int e4m3_ok, int gated) {
+// bf16 / e4m3), x itself for A16 tokens and 0 for absent rows; and s_x per
+// token (1 for A16 tokens, 0 for absent rows).  G = 128: the CTA loops over
+// the two 64-k halves with the same pair split (a thread owns 64 inputs).
+template <int KH>  // inputs per thread = G / 2
+__global__ void __launch_bounds__(2 * PT) actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
+                                                          const int32_t* __restrict__ row_bits, int bits,
+                                                          uint8_t* __restrict__ act, PreActLayout P, int64_t* err,
+                                                          int e4m3_ok, int gated) {
     ptx::pdl_wait();  // x / row_bits come from the preceding kernels
     ptx::pdl_launch_dependents();
-    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
     const int NG = L.NG, G = L.G;
-    const int TT = (M + PT - 1) / PT;
-    if (wid >= TT * PT * NG) return;
-    const int g = wid % NG;
-    const int row = (wid / NG) % PT;
-    const int tt = wid / (NG * PT);
-    const size_t tg = (size_t)tt * NG + g;
+    const int g = blockIdx.x % NG, tt = blockIdx.x / NG;
+    const int row = threadIdx.x >> 1, half = threadIdx.x & 1;
     const int m = tt * PT + row;
     const int b = m < M ? (row_bits ? row_bits[m] : bits) : 0;
     // tile mode (dyq_pre_tile_e4m3): every present token of tile tt at A2 / A4
-    int ok8 = e4m3_ok;
-    if (e4m3_ok)
-        for (int i = lane; i < PT; i += 32) {
-            const int mm = tt * PT + i;
-            const int bm = mm < M ? (row_bits ? row_bits[mm] : bits) : 2;
-            ok8 &= (bm == 2 || bm == 4);
-        }
-    const bool f8 = __all_sync(0xffffffffu, ok8) != 0;
+    const bool f8 = e4m3_ok && __syncthreads_and(m >= M || b == 2 || b == 4);
+    const size_t tg = (size_t)tt * NG + g;
+    if (threadIdx.x == 0 && g == 0) act[P.mode_off + tt] = f8 ? 1 : 0;  // read by the MMA kernel
     uint8_t* xg = act + P.x16_off + tg * P.x16_group;
-    auto x8_at = [&](int k) -> uint8_t* {  // e4m3 B operand: 32 k per K step, 32 B per row
-        const int ks = k >> 5, p = e4m3_kpos(k & 31);
-        return xg + ks * (PT * 32) + (row >> 3) * 256 + (p >> 4) * 128 + (row & 7) * 16 + (p & 15);
-    };
-    auto x16_at = [&](int k) -> uint16_t* {
-        const int ks = k >> 4, kk = k & 15;
-        return reinterpret_cast<uint16_t*>(xg + ks * (PT * 32) + (row >> 3) * 256 + (kk >> 3) * 128 + (row & 7) * 16 +
-                                           (kk & 7) * 2);
-    };
-    float* sxo = reinterpret_cast<float*>(act + P.par_off + tg * PAR_BYTES) + row;
-    const uint16_t* src = x + (size_t)m * L.K * (gated ? 2 : 1) + (size_t)g * G;  // gated: [g | u] rows
-    constexpr int MAXV = 4;
-    float v[MAXV];
-    uint16_t raw[MAXV];
+    const int k0 = half * KH;  // inputs k0 .. k0 + KH - 1
+    const uint16_t* src = x + (size_t)(m < M ? m : 0) * L.K * (gated ? 2 : 1) + (size_t)g * G + k0;  // gated: [g | u]
+    constexpr int NW = KH / 2;  // 32-bit words per thread
+    uint32_t raw[NW];
     float vmin = 0.f, vmax = 0.f;
     int bad = 0x7fffffff;
+    if (b != 0) {
 #pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
-        const int k = lane + 32 * i;
-        raw[i] = 0;
-        v[i] = 0.f;
-        if (k < G && b != 0) {
-            raw[i] = gated ? silu_mul_bf16(src[k], src[k + L.K]) : src[k];
-            v[i] = bf16_bits_to_float(raw[i]);
-            if (!finite_f(v[i])) bad = min(bad, k);
-            vmin = fminf(vmin, v[i]);
-            vmax = fmaxf(vmax, v[i]);
+        for (int i = 0; i < NW; i += 4) {
+            uint4 w4 = *reinterpret_cast<const uint4*>(src + 2 * i);
+            if (gated) {
+                const uint4 u4 = *reinterpret_cast<const uint4*>(src + L.K + 2 * i);
+                const uint32_t gw[4] = {w4.x, w4.y, w4.z, w4.w}, uw[4] = {u4.x, u4.y, u4.z, u4.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    o[e] = (uint32_t)silu_mul_bf16(gw[e] & 0xffffu, uw[e] & 0xffffu) |
+                           ((uint32_t)silu_mul_bf16(gw[e] >> 16, uw[e] >> 16) << 16);
+                w4 = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            raw[i] = w4.x;
+            raw[i + 1] = w4.y;
+            raw[i + 2] = w4.z;
+            raw[i + 3] = w4.w;
         }
-    }
-    bad = warp_min_i(bad);
-    if (bad != 0x7fffffff && lane == 0) report_nonfinite(err, (int64_t)m * L.K + (int64_t)g * G + bad);
-    if (b != 2 && b != 4 && b != 8) {
 #pragma unroll
-        for (int i = 0; i < MAXV; ++i) {
-            const int k = lane + 32 * i;
-            if (k < G) {
-                if (f8)
-                    *x8_at(k) = 0;  // absent row (an f8 tile has no A16 rows)
-                else
-                    *x16_at(k) = (b == 16) ? raw[i] : (uint16_t)0;
+        for (int i = 0; i < NW; ++i)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const float v = bf16_bits_to_float((uint16_t)(raw[i] >> (16 * hh)));
+                if (!finite_f(v)) bad = min(bad, k0 + 2 * i + hh);
+                vmin = fminf(vmin, v);
+                vmax = fmaxf(vmax, v);
+            }
+    }
+    // pair combine (lanes 2 row, 2 row + 1 are adjacent in the warp)
+    vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, 1));
+    vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, 1));
+    bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, 1));
+    if (bad != 0x7fffffff && half == 0) report_nonfinite(err, (int64_t)m * L.K + (int64_t)g * G + bad);
+    float* sxo = reinterpret_cast<float*>(act + P.par_off + tg * PAR_BYTES) + row;
+    const bool quant = b == 2 || b == 4 || b == 8;
+    float s = 1.f;
+    int z = 0;
+    if (quant) fit_params(vmin, vmax, b, &s, &z);
+    if (half == 0) *sxo = quant ? s : (b == 16 ? 1.f : 0.f);
+    // codes of this thread's inputs (as exact centred integers), then the
+    // layout-ordered 16-B stores
+    auto val = [&](int i, int hh) -> float {  // input k0 + 2i + hh
+        const uint16_t r = (uint16_t)(raw[i] >> (16 * hh));
+        if (quant) return (float)(quantize_one(bf16_bits_to_float(r), s, z, b, L.round_mode) - z);
+        return 0.f;
+    };
+    uint8_t* rowb = xg + (row >> 3) * 256 + (row & 7) * 16;
+    if (!f8) {
+        // bf16: this thread covers K steps ks = k0/16 .. (k0 + KH)/16 - 1
+#pragma unroll
+        for (int ks = 0; ks < KH / 16; ++ks) {
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) {  // kk >> 3
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int i = ks * 8 + kh * 4 + e;  // word index: k = k0 + 2i, 2i + 1
+                    if (b == 16) {
+                        o[e] = raw[i];
+                    } else if (quant) {
+                        const __nv_bfloat162 p2 = __floats2bfloat162_rn(val(i, 0), val(i, 1));  // |q - z| <= 255: exact
+                        o[e] = *reinterpret_cast<const uint32_t*>(&p2);
+                    } else {
+                        o[e] = 0;
+                    }
+                }
+                const int KS = (k0 >> 4) + ks;
+                *reinterpret_cast<uint4*>(rowb + KS * (PT * 32) + kh * 128) = make_uint4(o[0], o[1], o[2], o[3]);
             }
         }
-        if (lane == 0) *sxo = b == 16 ? 1.f : 0.f;
-        return;
-    }
-    vmin = warp_min(vmin);
-    vmax = warp_max(vmax);
-    float s;
-    int z;
-    fit_params(vmin, vmax, b, &s, &z);
+    } else {
+        // e4m3: one 32-k K step per thread half (G = 64), two for G = 128
 #pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
-        const int k = lane + 32 * i;
-        if (k < G) {
-            const int qv = quantize_one(v[i], s, z, b, L.round_mode);
-            if (f8)
-                *x8_at(k) = e4m3_of((float)(qv - z));  // |qv - z| <= 15: exact in e4m3
-            else
-                *x16_at(k) = __bfloat16_as_ushort(__float2bfloat16_rn((float)(qv - z)));  // |qv - z| <= 255: exact
+        for (int ks = 0; ks < KH / 32; ++ks) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {  // p >> 4
+                uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int pp = 0; pp < 16; ++pp) {
+                    const int p = 16 * c + pp;
+                    const int kl = (((p >> 2) & 1) << 4) | (((p >> 3) & 3) << 2) | (p & 3);  // e4m3_kpos^-1
+                    const int kt = ks * 32 + kl;  // input index within this thread
+                    const uint32_t q8 = quant ? (uint32_t)e4m3_of(val(kt >> 1, kt & 1)) : 0u;  // |q - z| <= 15
+                    o[pp >> 2] |= q8 << (8 * (pp & 3));
+                }
+                const int KS = (k0 >> 5) + ks;
+                *reinterpret_cast<uint4*>(rowb + KS * (PT * 32) + c * 128) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
         }
     }
-    if (lane == 0) *sxo = s;
 }
 
 // ------------------------------------------------------------------ host
@@ -643,7 +745,8 @@ PreActLayout pre_act_layout(const WLayout& L, int M) {
     P.x16_group = (size_t)(L.G / 16) * PT * 32;
     P.x16_off = 0;
     P.par_off = ((size_t)TT * L.NG * P.x16_group + 255) & ~(size_t)255;
-    P.bytes = P.par_off + (((size_t)TT * L.NG * PAR_BYTES + 255) & ~(size_t)255);
+    P.mode_off = P.par_off + (((size_t)TT * L.NG * PAR_BYTES + 255) & ~(size_t)255);
+    P.bytes = P.mode_off + (((size_t)TT + 255) & ~(size_t)255);
     return P;
 }
 
@@ -651,43 +754,19 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
                                  void* act, int64_t* err, cudaStream_t st, int gated) {
     const PreActLayout P = pre_act_layout(L, M);
     const int TT = (M + PT - 1) / PT;
-    const long long warps = (long long)TT * PT * L.NG;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)((warps * 32 + DYQ_AQP_THREADS - 1) / DYQ_AQP_THREADS));
-    cfg.blockDim = dim3(DYQ_AQP_THREADS);
+    cfg.gridDim = dim3((unsigned)(TT * L.NG));
+    cfg.blockDim = dim3(2 * PT);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, actquant_pre_kernel, L, x, M, row_bits, bits,
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, L.G == 64 ? actquant_pre_kernel<32> : actquant_pre_kernel<64>, L, x, M, row_bits, bits,
                                              reinterpret_cast<uint8_t*>(act), P, err, pre_e4m3_enabled(L) ? 1 : 0, gated);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "actquant_pre_kernel launch: %s", cudaGetErrorString(e));
     return check_launch("actquant_pre_kernel");
-}
-
-// y = sum_z part[z] in split order (deterministic), 4 outputs per thread.
-__global__ void split_reduce_kernel(const float* __restrict__ part, int ks, size_t MN, void* __restrict__ y,
-                                    int y_dtype) {
-    ptx::pdl_wait();
-    ptx::pdl_launch_dependents();
-    const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    if (i >= MN) return;
-    float4 acc = *reinterpret_cast<const float4*>(part + i);
-    for (int z = 1; z < ks; ++z) {
-        const float4 v = *reinterpret_cast<const float4*>(part + (size_t)z * MN + i);
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-    }
-    if (y_dtype == 0) {
-        *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + i) = acc;
-    } else {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
-        uint2 o;
-        o.x = *reinterpret_cast<uint32_t*>(&lo);
-        o.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(y) + i) = o;
-    }
 }
 
 static int sm_count() {
@@ -703,37 +782,45 @@ static int sm_count() {
     return sms;
 }
 
-// Split the K-groups over up to 4 CTAs per output tile when that shortens the
-// estimated wave schedule (o / down at M = 288: 64 CTAs on 148 SMs -> 2; qkv:
-// 192 CTAs -> 2; gate|up: 344 CTAs -> 1), keeping >= 8 groups per split.
-// DYQ_PRE_KSPLIT=k caps the split at k (1 disables).
-int prefill_ksplit(const WLayout& L, int M) {
-    static const int cap = [] {
-        const char* v = getenv("DYQ_PRE_KSPLIT");
-        return v ? atoi(v) : 4;
-    }();
+// Persistent stream-K grid: one CTA per SM (at most), each with a contiguous
+// range of >= DYQ_PRE_MIN_GROUPS K-groups of the flat (tile, token tile, group)
+// order.  DYQ_PRE_CTAS=n overrides the CTA count (experiments, tools/).
+static int prefill_grid(const WLayout& L, int M) {
     static const int force = [] {
-        const char* v = getenv("DYQ_PRE_KSPLIT_FORCE");  // experiments (tools/): fixed split
+        const char* v = getenv("DYQ_PRE_CTAS");
         return v ? atoi(v) : 0;
     }();
-    if (force > 0) return (L.NG / force >= 1) ? force : 1;
-    // waves x per-CTA time, the latter ~ NG / ks + 20 group times of fixed
-    // cost (fitted to the M = 288 o / down / qkv / gate|up measurements)
-    const int ctas = L.T128 * ((M + PT - 1) / PT), sms = sm_count();
-    int best = 1;
-    double best_t = 1e30;
-    for (int ks = 1; ks <= cap && ks <= 4 && L.NG / ks >= 8; ++ks) {
-        const double t = (double)((ctas * ks + sms - 1) / sms) * ((double)L.NG / ks + 20.0);
-        if (t < best_t - 1e-9) {
-            best_t = t;
-            best = ks;
-        }
+    const long long W = (long long)L.T128 * ((M + PT - 1) / PT) * L.NG;
+    long long P = force > 0 ? force : W / DYQ_PRE_MIN_GROUPS;
+    if (P > sm_count()) P = sm_count();  // all CTAs co-resident: a reducer may wait on any other CTA
+    if (P > W) P = W;
+    return (int)(P < 1 ? 1 : P);
+}
+
+size_t prefill_part_bytes(const WLayout& L, int M) {
+    return M > 0 ? (size_t)prefill_grid(L, M) * PT * 128 * sizeof(float) : 0;
+}
+
+// Largest number of CTAs sharing one (tile, token tile) unit (1 = no unit is
+// split across CTAs; dyq_qlinear_plan).
+int prefill_ksplit(const WLayout& L, int M) {
+    if (M <= 0) return 1;
+    const int P = prefill_grid(L, M);
+    const long long W = (long long)L.T128 * ((M + PT - 1) / PT) * L.NG;
+    int best = 1, run = 1;
+    long long prev_unit = -1;
+    for (int c = 1; c < P; ++c) {
+        const long long b = sk_begin(W, P, c);  // boundary between CTAs c-1 and c
+        if (b % L.NG == 0) continue;
+        run = (b / L.NG == prev_unit) ? run + 1 : 2;  // each mid-unit boundary adds a contributor
+        prev_unit = b / L.NG;
+        best = run > best ? run : best;
     }
     return best;
 }
 
 template <int WBITS, int SPG, bool PARTIALS, bool TP = false>
-static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
+static cudaError_t pre_launch(const PreArgs& a0, int grid, cudaStream_t st) {
     PreArgs a = a0;
     constexpr int G = SPG * 64;
     const int raw = SPG * 8 * 512 * (WBITS / 4);
@@ -741,12 +828,13 @@ static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
     a.off_meta = raw;
     a.off_b = (a.off_meta + META_BLOCK + 127) & ~127;
     a.off_par = a.off_b + bbytes;
-    a.off_a = 0;  // the A operand lives in TMEM
     a.stage_bytes = (a.off_par + PAR_BYTES + 127) & ~127;
-    a.stages = (220 * 1024) / a.stage_bytes;
+    constexpr int stg_bytes = PT * STG_ROW;
+    a.stages = (226 * 1024 - 1024 - stg_bytes) / a.stage_bytes;
     if (a.stages > DYQ_PRE_MAX_STAGES) a.stages = DYQ_PRE_MAX_STAGES;
     if (a.stages < 2) a.stages = 2;
-    const size_t smem = 1024 + (size_t)a.stages * a.stage_bytes;
+    a.off_stage = 1024 + a.stages * a.stage_bytes;
+    const size_t smem = (size_t)a.off_stage + stg_bytes;
     auto kern = qlinear_prefill_kernel<WBITS, SPG, PARTIALS, TP>;
     static bool attr = false;
     if (!attr) {
@@ -754,7 +842,7 @@ static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
+    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(PRE_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -767,7 +855,7 @@ static cudaError_t pre_launch(const PreArgs& a0, dim3 grid, cudaStream_t st) {
 }
 
 template <bool PARTIALS, bool TP = false>
-static cudaError_t pre_dispatch(const PreArgs& a, dim3 grid, cudaStream_t st) {
+static cudaError_t pre_dispatch(const PreArgs& a, int grid, cudaStream_t st) {
     if (a.L.wbits == 4)
         return a.L.G == 64 ? pre_launch<4, 1, PARTIALS, TP>(a, grid, st) : pre_launch<4, 2, PARTIALS, TP>(a, grid, st);
     return a.L.G == 64 ? pre_launch<8, 1, PARTIALS, TP>(a, grid, st) : pre_launch<8, 2, PARTIALS, TP>(a, grid, st);
@@ -776,6 +864,7 @@ static cudaError_t pre_dispatch(const PreArgs& a, dim3 grid, cudaStream_t st) {
 dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,
                             int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st,
                             const TpPeers* tp) {
+    if (M <= 0) return DYQ_OK;
     PreArgs a;
     a.L = L;
     a.codes = reinterpret_cast<const uint8_t*>(codes);
@@ -788,37 +877,21 @@ dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* met
     a.I_out = I_out;
     a.act = reinterpret_cast<const uint8_t*>(act);
     a.P = pre_act_layout(L, M);
-    a.e4m3 = pre_e4m3_enabled(L) ? 1 : 0;
-    a.trace = g_trace;
+    a.TT = (M + PT - 1) / PT;
+    a.W = (long long)L.T128 * a.TT * L.NG;
     a.tp = {};
     if (tp) a.tp = *tp;
-    // split-K applies to the integer partials too (each split writes its own
-    // groups of I_out, so the split path is bit-checked); the fp32 partial
-    // tiles live in the workspace, reserved only for M > 16
-    a.ksplit = (tp || M <= DEC_MPAD) ? 1 : prefill_ksplit(L, M);
+    // the fused TP epilogue announces whole units: one unit per CTA
+    const int grid = tp ? L.T128 * a.TT : prefill_grid(L, M);
     a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(const_cast<void*>(act)) +
                                       ((a.P.bytes + 255) & ~(size_t)255));
-    const dim3 grid(L.T128, (M + PT - 1) / PT, a.ksplit);
+    a.cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(const_cast<void*>(act)) - PRE_CNT_BYTES);
+    a.trace = g_trace;
+    a.serial = g_trace_serial++;
     const cudaError_t e = I_out ? pre_dispatch<true>(a, grid, st)
                           : tp  ? pre_dispatch<false, true>(a, grid, st)
                                 : pre_dispatch<false>(a, grid, st);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "qlinear_prefill_kernel launch: %s", cudaGetErrorString(e));
-    if (a.ksplit > 1 && !I_out) {
-        const size_t MN = (size_t)M * L.N;  // N % 16 == 0: whole float4 groups
-        const unsigned blocks = (unsigned)((MN / 4 + 255) / 256);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(blocks);
-        cfg.blockDim = dim3(256);
-        cfg.stream = st;
-        cudaLaunchAttribute attr1[1];
-        attr1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr1[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-        cfg.attrs = attr1;
-        cfg.numAttrs = 1;
-        const cudaError_t e2 = cudaLaunchKernelEx(&cfg, split_reduce_kernel, (const float*)a.part, a.ksplit, MN, y,
-                                                  y_dtype);
-        if (e2 != cudaSuccess) return set_error(DYQ_ECUDA, "split_reduce_kernel launch: %s", cudaGetErrorString(e2));
-    }
     return DYQ_OK;
 }
 

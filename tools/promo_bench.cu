@@ -176,9 +176,24 @@ __device__ __forceinline__ void l16_x1(uint32_t t, uint32_t* r) {
     asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(t));
 }
-template <int W, int NB, int SUBS>
-__global__ void __launch_bounds__(W * 32, 1) probe16(int iters, unsigned long long* out, float* sink) {
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((128 >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((256 >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+// MMAK: 0 none, 1 = one extra warp issues chained kind::f16 128x144x16 MMAs
+// (A from TMEM, B from smem) into TMEM columns [160, 304) while the
+// promotion warps run; 2 = kind::f8f6f4 (e4m3, K = 32)
+template <int W, int NB, int SUBS, int MMAK = 0>
+__global__ void __launch_bounds__(W * 32 + (MMAK ? 32 : 0), 1) probe16(int iters, unsigned long long* out, float* sink) {
     __shared__ uint32_t s_tmem;
+    __shared__ __align__(1024) uint8_t s_b[16384];
+    __shared__ volatile int s_done;
+    __shared__ unsigned long long s_nmma;
+    __shared__ __align__(8) unsigned long long s_bar;
     __shared__ __align__(16) float s_x[8][144];
     __shared__ __align__(16) float s_w[8][128];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -192,6 +207,48 @@ __global__ void __launch_bounds__(W * 32, 1) probe16(int iters, unsigned long lo
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) reinterpret_cast<uint32_t*>(s_b)[i] = 0;
+    if (threadIdx.x == 0) {
+        s_done = 0;
+        s_nmma = 0;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (MMAK && warp == W) {
+        // MMA issuer: chained 4-step groups until the promotion warps finish
+        const uint32_t d = s_tmem + 160, a = s_tmem + 400;
+        const uint64_t bd = sdesc((uint32_t)__cvta_generic_to_shared(s_b));
+        const uint32_t idesc = MMAK == 1 ? ((1u << 4) | (1u << 7) | (1u << 10) | ((144u >> 3) << 17) | ((128u >> 4) << 24))
+                                         : ((1u << 4) | ((144u >> 3) << 17) | ((128u >> 4) << 24));
+        unsigned long long n = 0;
+        while (!s_done) {
+            if (lane == 0) {
+                for (int k = 0; k < 4; ++k) {
+                    if (MMAK == 1)
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a + 8 * k), "l"(bd), "r"(idesc), "r"(k));
+                    else
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a + 8 * k), "l"(bd), "r"(idesc), "r"(k));
+                }
+                n += 4;
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            s_nmma = n;
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(&s_bar)) : "memory");
+            asm volatile("{\n\t.reg .pred P;\nW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t@!P bra W;\n\t}" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(&s_bar)) : "memory");
+        }
+        __syncwarp();
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        __syncthreads();
+        if (warp == 0) {}
+        return;
+    }
     const int q = warp & 3, c = warp >> 2;
     const int gid = lane >> 2, t = lane & 3;
     const int col0 = (c * NB * 8) % 144;
@@ -203,7 +260,8 @@ __global__ void __launch_bounds__(W * 32, 1) probe16(int iters, unsigned long lo
         for (int i = 0; i < NB; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[s][i][j] = 0.f;
-    __syncthreads();
+    if (MMAK) asm volatile("bar.sync 1, %0;" ::"r"(W * 32)); else __syncthreads();
+    
     const long long c0 = clock64();
     for (int it = 0; it < iters; ++it) {
         const int s = it & 7;
@@ -232,8 +290,14 @@ __global__ void __launch_bounds__(W * 32, 1) probe16(int iters, unsigned long lo
         }
     }
     const long long c1 = clock64();
+    if (MMAK) {
+        asm volatile("bar.sync 1, %0;" ::"r"(W * 32));
+        if (threadIdx.x == 0) s_done = 1;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (threadIdx.x == 0) out[blockIdx.x] = (unsigned long long)(c1 - c0);
+    if (threadIdx.x == 0 && MMAK) out[200 + blockIdx.x] = s_nmma;
     float tt = 0.f;
 #pragma unroll
     for (int s = 0; s < SUBS; ++s)
@@ -242,20 +306,25 @@ __global__ void __launch_bounds__(W * 32, 1) probe16(int iters, unsigned long lo
 #pragma unroll
             for (int j = 0; j < 4; ++j) tt += acc[s][i][j];
     sink[blockIdx.x * blockDim.x + threadIdx.x] = tt;
-    asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem));
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem));
+    }
 }
-template <int W, int NB, int SUBS>
+template <int W, int NB, int SUBS, int MMAK = 0>
 void run16(unsigned long long* d, float* sink) {
     const int iters = 4000;
-    probe16<W, NB, SUBS><<<148, W * 32>>>(iters, d, sink);
+    probe16<W, NB, SUBS, MMAK><<<148, W * 32 + (MMAK ? 32 : 0)>>>(iters, d, sink);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long c[148];
     cudaMemcpy(c, d, sizeof c, cudaMemcpyDeviceToHost);
     unsigned long long mx = 0;
     for (int i = 0; i < 148; ++i) mx = c[i] > mx ? c[i] : mx;
     const double elems = (double)W * 32 * NB * 4 * SUBS;  // per iteration per CTA
+    unsigned long long nm = 0;
+    if (MMAK) cudaMemcpy(&nm, d + 200, 8, cudaMemcpyDeviceToHost);
+    printf("mma=%d (%llu MMAs, %.1f clk each) ", MMAK, nm, nm ? (double)mx / nm : 0.0);
     printf("16x256b W=%2d NB=%d subs=%d: %.1f clk/iter, %.1f clk per 18432 elements (floor 288)  %s\n", W, NB, SUBS,
            (double)mx / iters, (double)mx / iters * 18432.0 / elems, cudaGetErrorString(e));
 }
@@ -270,9 +339,15 @@ int main2() {
     run16<12, 6, 2>(d, sink);
     run16<24, 3, 2>(d, sink);
     run16<16, 9, 1>(d, sink);
+    run16<8, 9, 2, 1>(d, sink);
+    run16<12, 6, 2, 1>(d, sink);
+    run16<16, 4, 2, 1>(d, sink);
+    run16<8, 9, 2, 2>(d, sink);
+    run16<12, 6, 2, 2>(d, sink);
     return 0;
 }
 int main() {
+    setvbuf(stdout, NULL, _IONBF, 0);
     main1();
     main2();
     return 0;

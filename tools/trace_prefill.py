@@ -1,8 +1,11 @@
-"""Per-group pipeline timeline of the prefill kernel, CTA (0,0), from the
-non-blocking trace (dyq_trace_enable; buffer slots 16 + 512 ev + g).
-usage: python tools/build_variant.py trace -DDYQ_PREFILL_TRACE=1
-       DYQ_LIB=tools/variants/libdyq_trace.so python tools/trace_prefill.py [linear] [M] [bits]
-(the product build compiles the per-group hooks out; DYQ_PRE_E4M3=1 for the e4m3 path)"""
+"""Per-CTA timeline of the persistent prefill kernel from the %globaltimer
+trace (dyq_trace_enable, kernel id 2).  Runs R back-to-back qlinear calls of
+one Llama linear (act-quant + prefill, as in the block step) inside a CUDA
+graph with tracing on, then prints per prefill launch (relative to the first
+CTA entry of that launch, us): CTA entry spread, promotion past
+griddepcontrol.wait, first accumulator ready, first / last segment end,
+epilogue + reducer wait, CTA exit.
+usage: python tools/trace_prefill.py [linear] [M] [bits] [R]"""
 import os
 import sys
 
@@ -16,28 +19,64 @@ from paper_2603_07904_b200 import dyq  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "gate_up"
 M = int(sys.argv[2]) if len(sys.argv) > 2 else 288
 bits = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+R = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 N, K = {n: (N, K) for n, N, K in synth.LLAMA_BLOCK_LINEARS}[name]
 dev = "cuda:0"
-p = dyq.PackedLinear.from_bf16(synth.weights_bf16_torch(N, K, seed=1, device=dev), group=64, wbits=4)
+ps = [dyq.PackedLinear.from_bf16(synth.weights_bf16_torch(N, K, seed=1 + c, device=dev), group=64, wbits=4)
+      for c in range(2)]
 x = synth.activations_bf16_torch(M, K, seed=1000, device=dev)
 y = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
-ws = p.workspace(M)
+ws = ps[0].workspace(M)
 for _ in range(3):
-    dyq.qlinear(p.wd, p.codes, p.meta, x, M, None, bits, y, 1, ws)
+    dyq.qlinear(ps[0].wd, ps[0].codes, ps[0].meta, x, M, None, bits, y, 1, ws)
 torch.cuda.synchronize()
-tr = torch.zeros(1 << 14, dtype=torch.int64, device=dev)
+tr = torch.zeros(1 << 20, dtype=torch.int64, device=dev)
 dyq.trace_enable(tr)
-dyq.qlinear(p.wd, p.codes, p.meta, x, M, None, bits, y, 1, ws)
-torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+with torch.cuda.graph(g, stream=s):
+    for r in range(R):
+        p = ps[r % 2]
+        dyq.qlinear(p.wd, p.codes, p.meta, x, M, None, bits, y, 1, ws)
 dyq.trace_enable(None)
-raw = tr.cpu().numpy().astype(np.int64)
-NG = K // 64
-ev = {e: raw[16 + 512 * e: 16 + 512 * e + NG] for e in range(1, 8)}
-t0 = ev[1].min()
-names = {1: "issued", 2: "B_landed", 3: "A_ready", 4: "acc_free", 5: "xf_done", 6: "pr_start", 7: "pr_done"}
-print("group " + " ".join(f"{names[e]:>9}" for e in range(1, 8)) + "   (us, CTA (0,0))")
-for g in list(range(8)) + list(range(NG - 4, NG)):
-    print(f"{g:5d} " + " ".join(f"{(ev[e][g] - t0) / 1e3:9.2f}" for e in range(1, 8)))
-d = lambda a, b: np.median((ev[b][8:] - ev[a][8:]) / 1e3)  # noqa: E731
-print(f"median per group: cadence {np.median(np.diff(ev[6][8:])) / 1e3:.3f} us; acc_free->pr_start (MMA+commit) "
-      f"{d(4, 6):.3f}; pr_start->pr_done {d(6, 7):.3f}; B_landed-issued {d(1, 2):.3f}")
+torch.cuda.synchronize()
+tr.zero_()
+tr[1] = (tr.numel() * 8 - 16) // 16
+g.replay()
+torch.cuda.synchronize()
+t = tr.cpu().numpy().view(np.uint64)
+n = int(t[0])
+rec = t[2:2 + 2 * n].reshape(-1, 2)
+tag, ns = rec[:, 0], rec[:, 1].astype(np.int64)
+serial = (tag >> 32).astype(np.int64)
+kern = ((tag >> 24) & 0xff).astype(np.int64)
+ev = ((tag >> 16) & 0xff).astype(np.int64)
+cta = (tag & 0xffff).astype(np.int64)
+sel = kern == 2
+t0g = ns[sel].min() if sel.any() else 0
+prev_end = None
+for sr in sorted(set(serial[sel].tolist())):
+    m = sel & (serial == sr)
+    base = ns[m & (ev == 0)].min()
+
+    def q(e, f=np.median):
+        v = ns[m & (ev == e)]
+        return f(v - base) / 1e3 if len(v) else float("nan")
+    e4 = ns[m & (ev == 4)]
+    e3 = ns[m & (ev == 3)]
+    line = (f"launch {sr}: start {(base - t0g) / 1e3:8.1f}  gap {(base - prev_end) / 1e3 if prev_end else 0:6.1f} | "
+            f"entry spread {q(0, np.max):6.1f}  pdl-wait done {q(1):6.1f}  first acc {q(2):6.1f} / max {q(2, np.max):6.1f} | "
+            f"seg end med {q(3):6.1f}  epi done med {q(4):6.1f}  max {q(4, np.max):6.1f} | exit max {q(5, np.max):6.1f}")
+    print(line)
+    # epilogue cost per segment (ev4 - ev3 pairs, per CTA in order)
+    d = []
+    for c in set(cta[m].tolist()):
+        a3 = np.sort(ns[m & (ev == 3) & (cta == c)])
+        a4 = np.sort(ns[m & (ev == 4) & (cta == c)])
+        d += list((a4 - a3)[: min(len(a3), len(a4))])
+    if d:
+        d = np.array(d) / 1e3
+        print(f"           epilogue (ev4 - ev3) per segment: median {np.median(d):.2f} us, max {d.max():.2f} us, "
+              f"n {len(d)}")
+    prev_end = ns[m & (ev == 5)].max()
