@@ -792,8 +792,8 @@ def policy_slice(args, dyq, synth, torch, dev, packed, C, rank, world, graph_of,
     embed = synth.activations_bf16_torch(32000, d_m, seed=7000, device=dev)
     head = synth.weights_bf16_torch(256, d_m, seed=7001, device=dev)
 
-    def run(E, eps_seed):
-        model = dyq.Model(layers, norms, norms, one, embed, head, E=E, n_heads=32)
+    def run(E, eps_seed, **mkw):
+        model = dyq.Model(layers, norms, norms, one, embed, head, E=E, n_heads=32, **mkw)
         cal = dyq.default_calib()
         pst = torch.zeros(dyq.state_size(E, cal), dtype=torch.uint8, device=dev)
         dyq.state_init(E, cal, pst)
@@ -825,6 +825,13 @@ def policy_slice(args, dyq, synth, torch, dev, packed, C, rank, world, graph_of,
             ms = run(E, 7100 + rank)
             pres[f"E{E}"] = {"episodes_per_gpu": E, "ms_per_step": round(ms, 3),
                             "policy_steps_per_s": round(E / (ms * 1e-3), 2)}
+        # paper mode: selector on a side stream overlapping the
+        # prefill, prefill at BF16, decode at b*_t
+        ms = run(1, 7100 + rank, paper_mode=1, prefill_bits=16)
+        pres["E1_paper_mode"] = {"episodes_per_gpu": 1, "ms_per_step": round(ms, 3),
+                                 "policy_steps_per_s": round(1 / (ms * 1e-3), 2),
+                                 "what": "dyq_policy_step paper_mode=1: prefill at BF16 (fixed), select_bits on a "
+                                         "forked stream joined before the decode passes"}
     Et = args.policy_E_total
     mine = episodes.shard(Et, world, rank)
     ms = run(len(mine), 7100 + mine.start) if len(mine) else 0.0

@@ -26,7 +26,8 @@
  *    offending index") cannot be detected synchronously on a stream: kernels
  *    atomicMin the smallest offending linear element index into the caller's
  *    device int64 `err` (initialise it with dyq_error_reset; INT64_MAX = none)
- *    and the caller polls it (dyq_error_read).  Outputs derived from
+ *    and the caller polls it (dyq_check_error, non-blocking; dyq_error_read
+ *    synchronizes).  Outputs derived from
  *    non-finite inputs are unspecified.  `err` may be NULL (no reporting).
  *  - Packed weights are immutable after packing and may be shared by any
  *    number of streams.  Selection state is single-owner and mutated in step
@@ -80,6 +81,14 @@ DYQ_API dyq_status_t dyq_error_reset(int64_t* err, dyq_stream_t stream);
 /* Synchronizes `stream` and copies *err to *host_index (INT64_MAX = none).
  * Returns DYQ_ENONFINITE if an index was recorded.  (Debug / test path.) */
 DYQ_API dyq_status_t dyq_error_read(const int64_t* err, int64_t* host_index, dyq_stream_t stream);
+/* Non-blocking poll of *err (SURVEY §8(b) dyq_check_error): the first call
+ * for `err` enqueues an async device->host copy into a library-owned pinned
+ * slot plus an event on `stream` and returns at once; every call queries the
+ * event without waiting.  While the copy is in flight: DYQ_OK with
+ * *host_index = -1.  Once it has landed: *host_index = the recorded value
+ * (INT64_MAX = none), DYQ_ENONFINITE if an index was recorded, else DYQ_OK;
+ * the next call re-arms a fresh copy.  Never synchronizes the stream. */
+DYQ_API dyq_status_t dyq_check_error(const int64_t* err, int64_t* host_index, dyq_stream_t stream);
 
 /* ------------------------------------------------------------ weight pack */
 /* Weight descriptor.  One (scale, zero-point) per output row n and per group
@@ -252,6 +261,17 @@ DYQ_API dyq_status_t dyq_act_quant_for_check(const dyq_wdesc_t* wd, const uint16
  * 1 = decode (M <= 64 only), 2 = prefill.  Process-wide. */
 DYQ_API dyq_status_t dyq_set_path(int32_t path);
 
+/* dyq_qlinear with device-side masking (the variant table's building block):
+ * rows m with row_bits[m] == 0 are not computed into y (y rows left as they
+ * were), and if gate != NULL and *gate == 0 at execution time every kernel of
+ * the call returns immediately (no weight bytes are read).  row_bits must be
+ * non-NULL.  Lets two calls on different weight copies (W4 / W8) share one
+ * output, each owning its rows, with the choice made on the device. */
+DYQ_API dyq_status_t dyq_qlinear_masked(const dyq_wdesc_t* wd, const void* codes, const void* meta,
+                                        const uint16_t* x, int32_t M, const int32_t* row_bits,
+                                        const int32_t* gate, void* y, int32_t y_dtype, void* workspace,
+                                        size_t ws_bytes, int64_t* err, dyq_stream_t stream);
+
 /* ============================================================ policy step
  * one VLA control step around the quantized linears.  The
  * backbone is OpenVLA's Llama-2: n_vis vision embeddings (synthetic
@@ -282,6 +302,26 @@ typedef struct {
     const uint16_t* head_bins;  /* device bf16 [n_bins, d]: LM-head rows of the bin tokens */
     void* kv;                   /* device, kv_bytes: [E][n_layers][2][T][d] bf16, T = n_vis+n_text+n_act */
     void* scratch;              /* device, scratch_bytes (activations, qlinear workspace, ...)  */
+    /* ---- optional (all-zero = the paper's defaults) ----
+     * Variant table (P:221 pins the default to INT4): b*_t in
+     * {2, 4, 8, 16} (index 0..3) selects a weight copy wbits_of[i] in {4, 8}
+     * and activation bits abits_of[i].  A step's rows are routed per episode
+     * to the W4 or the W8 copy (codes_w8 / meta_w8: same order as codes,
+     * packed with wbits = 8 and the same group); each linear runs once per
+     * copy with the other copy's rows masked, and a copy with no live row is
+     * skipped on the device (dyq_qlinear_masked) -- a precision switch is a
+     * pointer + kernel-variant choice made on the GPU, with no host round trip.
+     * wbits_of all 0 -> {4,4,4,4}; abits_of all 0 -> {2,4,8,16}. */
+    const void* const* codes_w8; /* host array [n_layers * 4] or NULL (W4 only)        */
+    const void* const* meta_w8;
+    int32_t wbits_of[4];
+    int32_t abits_of[4];
+    /* Paper mode (§V-B): 1 = b*_t is selected on a side stream that
+     * overlaps the visual prefill (joined by an event before the decode
+     * passes); the prefill runs at prefill_bits on the W4 copy, the decode
+     * passes at b*_t.  0 (default): b*_t also switches the prefill. */
+    int32_t paper_mode;
+    int32_t prefill_bits;        /* paper_mode prefill activation bits; 0 -> 16 (BF16) */
 } dyq_model_desc_t;
 DYQ_API dyq_status_t dyq_model_size(const dyq_model_desc_t* desc, size_t* kv_bytes, size_t* scratch_bytes);
 DYQ_API dyq_status_t dyq_model_bind(const dyq_model_desc_t* desc, void** model);

@@ -108,9 +108,17 @@ class TinyModel:
     def __init__(self, w, G, wbits, n_heads, n_vis, n_text, n_act, eps=1e-5, theta=10000.0):
         self.w, self.G, self.wbits = w, G, wbits
         self.packs = [[o_pack(lin, G, wbits) for lin in layer] for layer in w["lin"]]
+        self._packs_by_w = {wbits: self.packs}
         self.H, self.n_vis, self.n_text, self.n_act = n_heads, n_vis, n_text, n_act
         self.eps, self.theta = eps, theta
         self.d = w["embed"].shape[1]
+
+    def use_wbits(self, wbits):
+        """Select the weight copy the next blocks run on (the variant table's
+        W4 / W8 copies of the same bf16 weights, each packed by Eq. 2)."""
+        if wbits not in self._packs_by_w:
+            self._packs_by_w[wbits] = [[o_pack(lin, self.G, wbits) for lin in layer] for layer in self.w["lin"]]
+        self.packs = self._packs_by_w[wbits]
 
     def _lin(self, l, i, x_bits, abits):
         y, _ = o_qlinear(x_bits, self.packs[l][i], self.G, abits)
@@ -140,11 +148,17 @@ class TinyModel:
         xn = bf16_round(rmsnorm(h, from_bf16_bits(nw), self.eps))
         return h, xn
 
-    def episode(self, vis_bits, text_ids, abits, forced=None):
+    def episode(self, vis_bits, text_ids, abits, forced=None, wbits=None, prefill=None):
         """One policy step of one episode at activation bits `abits` for every
         row.  Returns (tokens [n_act], logits [n_act, n_bins]).  `forced`
         (teacher forcing): decode pass i consumes forced[i-1] instead of the
-        reference's own previous token."""
+        reference's own previous token.  `wbits`: weight copy of the step
+        (variant table; default the constructor's); `prefill` = (abits,
+        wbits) of the prefill rows when they differ from the decode passes
+        (paper mode)."""
+        wb = self.wbits if wbits is None else wbits
+        pa, pw = (abits, wb) if prefill is None else prefill
+        self.use_wbits(pw)
         w = self.w
         L = len(self.packs)
         h = np.concatenate([from_bf16_bits(vis_bits), from_bf16_bits(w["embed"][text_ids])])
@@ -153,7 +167,8 @@ class TinyModel:
         kc, vc = [None] * L, [None] * L
         pos = np.arange(S)
         for l in range(L):
-            h, xn = self._layer(l, h, xn, kc, vc, pos, abits)
+            h, xn = self._layer(l, h, xn, kc, vc, pos, pa)
+        self.use_wbits(wb)
         head = from_bf16_bits(w["head"])
         n_bins, V = head.shape[0], w["embed"].shape[0]
         toks, logs = [], []
@@ -170,4 +185,5 @@ class TinyModel:
             lg, t = head_argmax(xn, head)
             toks.append(int(t[0]))
             logs.append(lg[0])
+        self.use_wbits(self.wbits)
         return np.array(toks), np.array(logs)

@@ -16,7 +16,9 @@ namespace dyq {
 // in x16; padding rows (m >= M): all zero.
 __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, int M, int m0,
                                     const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ ws,
-                                    ActLayoutDec A, int64_t* err, uint64_t* trace, uint32_t serial, int gated) {
+                                    ActLayoutDec A, int64_t* err, uint64_t* trace, uint32_t serial, int gated,
+                                    const int32_t* gate) {
+    if (gate_closed(gate)) return;
     ptx::pdl_launch_dependents();
     if (threadIdx.x == 0) trace_ev(trace, serial, 2, 0);
     ptx::pdl_wait();  // x may be produced by the preceding kernel
@@ -113,7 +115,7 @@ dyq_status_t launch_actquant_dec(const WLayout& L, const uint16_t* x, int M, int
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, actquant_dec_kernel, L, x, M, m0, row_bits, bits,
-                                             reinterpret_cast<uint8_t*>(ws), A, err, g_trace, g_trace_serial++, gated);
+                                             reinterpret_cast<uint8_t*>(ws), A, err, g_trace, g_trace_serial++, gated, g_gate);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "actquant_dec_kernel launch: %s", cudaGetErrorString(e));
     return check_launch("actquant_dec_kernel");
 }

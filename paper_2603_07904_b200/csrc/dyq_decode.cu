@@ -64,6 +64,7 @@ struct DecArgs {
     int stages, stage_bytes;
     int off_meta, off_cp, off_x16;  // offsets inside a stage
     uint64_t* trace;                // dyq_trace_enable buffer or null
+    const int32_t* gate;            // dyq_qlinear_masked gate or null
     uint32_t serial;
     TpPeers tp;                     // fused TP epilogue (tp.n = 0: off)
 };
@@ -205,6 +206,7 @@ __device__ __forceinline__ void dec_flush_warp(const DecArgs& a, int tile, const
     const int nc = c_last - c_first + 1;
     const int c = (int)blockIdx.x - c_first;
     auto store = [&](int tok, int r, float v) {
+        if (a.row_bits && a.row_bits[a.m0 + tok] == 0) return;  // masked row: y untouched
         if constexpr (TP) {  // every rank's full y, this rank's columns
             const size_t o = (size_t)(a.m0 + tok) * a.tp.ldy + a.tp.col0 + tile * 128 + sub * 16 + r;
             const __nv_bfloat16 h = __float2bfloat16_rn(v);
@@ -558,6 +560,7 @@ __global__ void __launch_bounds__(DEC_THREADS, NT8 == 1 ? DEC_MINB : 1) qlinear_
     constexpr int G = SPG * 64;
     constexpr int CPS = NT8 * 8 * G + NT8 * 64;
     constexpr int X16S = NT8 * 8 * G * 2;
+    if (gate_closed(a.gate)) return;
     const int U = L.T128 * NG;
     const int u0 = blockIdx.x * a.upc;
     const int u1 = min(U, u0 + a.upc);
@@ -839,6 +842,7 @@ dyq_status_t launch_decode(const WLayout& L, const void* codes, const void* meta
     a.off_x16 = p.off_x16;
     a.trace = g_trace;
     a.serial = g_trace_serial++;
+    a.gate = g_gate;
     a.tp = {};
     if (tp) a.tp = *tp;
     const bool partials = I_out != nullptr;

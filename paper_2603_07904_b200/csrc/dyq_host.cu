@@ -1,3 +1,5 @@
+#include <mutex>
+#include <unordered_map>
 // dyq_host.cu -- the C ABI of include/dyq.h: argument validation, sizing, plans
 // and kernel routing.  No allocation, no host synchronization on the hot path.
 #include <stdarg.h>
@@ -13,6 +15,7 @@ namespace dyq {
 
 static thread_local char g_err[512] = "";
 int g_path = 0;
+thread_local const int32_t* g_gate = nullptr;
 uint64_t* g_trace = nullptr;
 uint32_t g_trace_serial = 0;  // 0 auto, 1 decode, 2 prefill (read by the router)
 
@@ -113,6 +116,43 @@ dyq_status_t dyq_error_read(const int64_t* err, int64_t* host_index, dyq_stream_
     if (cudaMemcpyAsync(&v, err, sizeof v, cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess ||
         cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
         return check_launch("dyq_error_read");
+    *host_index = v;
+    if (v != INT64_MAX) return set_error(DYQ_ENONFINITE, "non-finite input at linear index %lld", (long long)v);
+    return DYQ_OK;
+}
+
+dyq_status_t dyq_check_error(const int64_t* err, int64_t* host_index, dyq_stream_t stream) {
+    if (!err || !host_index) return set_error(DYQ_EINVAL, "null pointer");
+    struct Poll {
+        int64_t* slot = nullptr;  // pinned host
+        cudaEvent_t ev = nullptr;
+        bool pending = false;
+    };
+    static std::mutex mu;
+    static std::unordered_map<const int64_t*, Poll> polls;
+    std::lock_guard<std::mutex> lock(mu);
+    Poll& p = polls[err];
+    if (!p.slot) {
+        if (cudaHostAlloc(reinterpret_cast<void**>(&p.slot), sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming) != cudaSuccess) {
+            polls.erase(err);
+            return check_launch("dyq_check_error (pinned slot)");
+        }
+    }
+    if (!p.pending) {
+        if (cudaMemcpyAsync(p.slot, err, sizeof(int64_t), cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess ||
+            cudaEventRecord(p.ev, (cudaStream_t)stream) != cudaSuccess)
+            return check_launch("dyq_check_error");
+        p.pending = true;
+    }
+    const cudaError_t q = cudaEventQuery(p.ev);
+    if (q == cudaErrorNotReady) {
+        *host_index = -1;
+        return DYQ_OK;
+    }
+    if (q != cudaSuccess) return check_launch("dyq_check_error (event)");
+    p.pending = false;
+    const int64_t v = *reinterpret_cast<volatile int64_t*>(p.slot);
     *host_index = v;
     if (v != INT64_MAX) return set_error(DYQ_ENONFINITE, "non-finite input at linear index %lld", (long long)v);
     return DYQ_OK;
@@ -242,6 +282,16 @@ dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* byt
     if (M > 0) pre = ((pre_act_layout(L, M).bytes + 255) & ~(size_t)255) + prefill_part_bytes(L, M);
     *bytes = prefill_area_offset(L) + pre;
     return DYQ_OK;
+}
+
+dyq_status_t dyq_qlinear_masked(const dyq_wdesc_t* wd, const void* codes, const void* meta, const uint16_t* x,
+                                int32_t M, const int32_t* row_bits, const int32_t* gate, void* y, int32_t y_dtype,
+                                void* workspace, size_t ws_bytes, int64_t* err, dyq_stream_t stream) {
+    if (!row_bits) return set_error(DYQ_EINVAL, "dyq_qlinear_masked needs row_bits");
+    g_gate = gate;
+    const dyq_status_t rc = dyq_qlinear(wd, codes, meta, x, M, row_bits, 0, y, y_dtype, workspace, ws_bytes, err, stream);
+    g_gate = nullptr;
+    return rc;
 }
 
 dyq_status_t dyq_qlinear_plan(const dyq_wdesc_t* wd, int32_t M, int32_t* path, int32_t* ksplit) {

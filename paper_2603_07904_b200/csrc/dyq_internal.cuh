@@ -236,6 +236,15 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
 dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* meta, int M, const int32_t* row_bits,
                             int bits, void* y, int y_dtype, int32_t* I_out, const void* act, cudaStream_t st, const TpPeers* tp = nullptr);
 extern int g_path;
+// Device gate of the current masked qlinear call (dyq_qlinear_masked): when
+// non-null every kernel of the call waits for its predecessors, reads *gate and
+// returns at once if it is 0 (no row of this call is live), before any copy.
+extern thread_local const int32_t* g_gate;
+__device__ __forceinline__ bool gate_closed(const int32_t* gate) {
+    if (!gate) return false;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return *reinterpret_cast<const volatile int32_t*>(gate) == 0;
+}
 // dyq_select.cu
 size_t sel_state_bytes(int32_t E, const dyq_calib_t& c);
 dyq_status_t launch_sel_init(int32_t E, const dyq_calib_t& c, void* state, cudaStream_t st);

@@ -757,19 +757,59 @@ __global__ void detok_kernel(const int32_t* __restrict__ tok, int E, int n_act, 
     if (bits_out && i < E) bits_out[i] = bits[i];
 }
 
+// Variant-table routing (dyq_model_desc_t wbits_of / abits_of): per row of
+// episode e = r / tpe, b*_e -> (weight copy, activation bits); rows of the
+// other copy get 0 (masked), and gates[c] = 1 iff copy c (0: W4, 1: W8) has a
+// live row.  One CTA.
+__global__ void variant_route_kernel(const int32_t* __restrict__ bits, int E, int tpe, int4 wtab, int4 atab,
+                                     int32_t* __restrict__ rb4, int32_t* __restrict__ rb8, int32_t* __restrict__ gates) {
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    __shared__ int any4, any8;
+    if (threadIdx.x == 0) any4 = any8 = 0;
+    __syncthreads();
+    const int wt[4] = {wtab.x, wtab.y, wtab.z, wtab.w}, at[4] = {atab.x, atab.y, atab.z, atab.w};
+    int a4 = 0, a8 = 0;
+    for (int r = threadIdx.x; r < E * tpe; r += blockDim.x) {
+        const int b = bits[r / tpe];
+        const int i = b == 2 ? 0 : b == 4 ? 1 : b == 8 ? 2 : 3;
+        const bool w8 = wt[i] == 8;
+        rb4[r] = w8 ? 0 : at[i];
+        rb8[r] = w8 ? at[i] : 0;
+        a4 |= !w8;
+        a8 |= w8;
+    }
+    if (a4) any4 = 1;
+    if (a8) any8 = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        gates[0] = any4;
+        gates[1] = any8;
+    }
+}
+
+__global__ void fill_i32_kernel(int32_t* __restrict__ p, int n, int v) {
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
+}
+
 // ------------------------------------------------------------------ host
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct ModelLayout {
     int S, T, MP;
-    size_t h, xn, delta, att, qkv, gu, act, ws[4], rbp, rbd, bits, tok, prev, logits, err, total;
-    size_t ws_bytes[4], kv_bytes;  // one qlinear workspace per linear shape (split-K counters are per shape)
+    size_t h, xn, delta, att, qkv, gu, act, ws[8], rbp, rbd, bits, tok, prev, logits, err, total;
+    size_t rb8p, rb8d, gates;      // variant table: W8 rows (prefill / decode), gates [W4p, W8p, W4d, W8d]
+    size_t ws_bytes[8], kv_bytes;  // one qlinear workspace per linear shape (split-K counters are per shape); 4-7: W8
+    bool w8;
 };
 
 static dyq_wdesc_t wdesc_of(const dyq_model_desc_t& m, int which) {
     dyq_wdesc_t w{};
     w.group = m.group;
-    w.wbits = m.wbits;
+    w.wbits = which >= 4 ? 8 : m.wbits;
+    which &= 3;
     w.round_mode = 0;
     switch (which) {
         case 0: w.N = 3 * m.d; w.K = m.d; break;
@@ -794,7 +834,21 @@ static dyq_status_t model_layout(const dyq_model_desc_t* m, ModelLayout* L) {
     L->MP = m->E * L->S;
     if (L->MP > 65536) return set_error(DYQ_ESHAPE, "E * (n_vis + n_text) must be <= 65536");
     const size_t MP = L->MP, d = m->d, ffn = m->ffn;
-    for (int which = 0; which < 4; ++which) {
+    L->w8 = m->codes_w8 != nullptr;
+    if (L->w8 && (!m->meta_w8 || m->wbits != 4)) return set_error(DYQ_EINVAL, "W8 table needs meta_w8 and W4 codes");
+    for (int i = 0; i < 4; ++i) {
+        if (m->wbits_of[i] != 0 && m->wbits_of[i] != 4 && m->wbits_of[i] != 8)
+            return set_error(DYQ_EINVAL, "wbits_of[%d] must be 4 or 8", i);
+        if (m->wbits_of[i] == 8 && !L->w8) return set_error(DYQ_EINVAL, "wbits_of[%d] = 8 without W8 copies", i);
+        const int a = m->abits_of[i];
+        if (a != 0 && a != 2 && a != 4 && a != 8 && a != 16) return set_error(DYQ_EINVAL, "abits_of[%d] = %d", i, a);
+    }
+    if (m->prefill_bits != 0 && m->prefill_bits != 2 && m->prefill_bits != 4 && m->prefill_bits != 8 &&
+        m->prefill_bits != 16)
+        return set_error(DYQ_EINVAL, "prefill_bits must be 0, 2, 4, 8 or 16");
+    const int nshapes = L->w8 ? 8 : 4;
+    for (int which = 4; which < 8; ++which) L->ws_bytes[which] = 0;
+    for (int which = 0; which < nshapes; ++which) {
         const dyq_wdesc_t w = wdesc_of(*m, which);
         // a step may run any e <= desc.E episodes (prefill M = e * S, decode
         // M = e) and the prefill split factor is not monotone in M, so the
@@ -818,9 +872,12 @@ static dyq_status_t model_layout(const dyq_model_desc_t* m, ModelLayout* L) {
     L->qkv = take(MP * 3 * d * 2);
     L->gu = take(MP * 2 * ffn * 2);
     L->act = take(MP * ffn * 2);
-    for (int which = 0; which < 4; ++which) L->ws[which] = take(L->ws_bytes[which]);
+    for (int which = 0; which < 8; ++which) L->ws[which] = take(L->ws_bytes[which]);
     L->rbp = take(MP * 4);
     L->rbd = take((size_t)m->E * 4);
+    L->rb8p = take(MP * 4);
+    L->rb8d = take((size_t)m->E * 4);
+    L->gates = take(16);
     L->bits = take((size_t)m->E * 4);
     L->tok = take((size_t)m->E * m->n_act * 4);
     L->prev = take((size_t)m->E * 7 * 4);
@@ -833,7 +890,9 @@ static dyq_status_t model_layout(const dyq_model_desc_t* m, ModelLayout* L) {
 
 struct Model {
     dyq_model_desc_t d;
-    std::vector<const void*> codes, meta;
+    std::vector<const void*> codes, meta, codes8, meta8;
+    cudaStream_t side = nullptr;  // paper mode: the selector's stream
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ModelLayout L;
     int t = 0;
     uint8_t* sb() const { return reinterpret_cast<uint8_t*>(d.scratch); }
@@ -979,8 +1038,26 @@ dyq_status_t dyq_model_bind(const dyq_model_desc_t* desc, void** model) {
             delete m;
             return set_error(DYQ_EINVAL, "null packed-weight pointer for linear %d", i);
         }
+    if (L.w8) {
+        m->codes8.assign(desc->codes_w8, desc->codes_w8 + 4 * desc->n_layers);
+        m->meta8.assign(desc->meta_w8, desc->meta_w8 + 4 * desc->n_layers);
+        for (int i = 0; i < 4 * desc->n_layers; ++i)
+            if (!m->codes8[i] || !m->meta8[i]) {
+                delete m;
+                return set_error(DYQ_EINVAL, "null W8 packed-weight pointer for linear %d", i);
+            }
+    }
+    if (desc->paper_mode &&
+        (cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+        delete m;
+        return check_launch("dyq_model_bind (paper-mode stream)");
+    }
     m->d.codes = nullptr;
     m->d.meta = nullptr;
+    m->d.codes_w8 = nullptr;
+    m->d.meta_w8 = nullptr;
     m->L = L;
     *model = m;
     return DYQ_OK;
@@ -996,7 +1073,13 @@ dyq_status_t dyq_model_init(void* model, dyq_stream_t stream) {
 }
 
 dyq_status_t dyq_model_free(void* model) {
-    delete reinterpret_cast<Model*>(model);
+    Model* m = reinterpret_cast<Model*>(model);
+    if (m && m->side) {
+        cudaStreamDestroy(m->side);
+        cudaEventDestroy(m->ev_fork);
+        cudaEventDestroy(m->ev_join);
+    }
+    delete m;
     return DYQ_OK;
 }
 
@@ -1037,38 +1120,102 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
         rc = (x);         \
         if (rc) return rc; \
     } while (0)
-    dyq_wdesc_t wd[4];
-    for (int i = 0; i < 4; ++i) wd[i] = wdesc_of(D, i);
+    dyq_wdesc_t wd[8];
+    for (int i = 0; i < 8; ++i) wd[i] = wdesc_of(D, i);
+    void* ws8[4];
+    for (int i = 0; i < 4; ++i) ws8[i] = m->at<uint8_t>(L.ws[4 + i]);
+    int32_t* rb8p = m->at<int32_t>(L.rb8p);
+    int32_t* rb8d = m->at<int32_t>(L.rb8d);
+    int32_t* gates = m->at<int32_t>(L.gates);  // [W4 prefill, W8 prefill, W4 decode, W8 decode]
+    const bool w8 = L.w8 && !forced;           // forced-bits steps (calibration) stay on the W4 table
+    const bool paper = D.paper_mode && !forced && m->side;
+    const int pre_bits = D.prefill_bits ? D.prefill_bits : 16;
+    int4 wtab = make_int4(4, 4, 4, 4), atab = make_int4(2, 4, 8, 16);
+    if (D.wbits_of[0] | D.wbits_of[1] | D.wbits_of[2] | D.wbits_of[3])
+        wtab = make_int4(D.wbits_of[0] ? D.wbits_of[0] : 4, D.wbits_of[1] ? D.wbits_of[1] : 4,
+                         D.wbits_of[2] ? D.wbits_of[2] : 4, D.wbits_of[3] ? D.wbits_of[3] : 4);
+    const bool atab_set = D.abits_of[0] | D.abits_of[1] | D.abits_of[2] | D.abits_of[3];
+    if (atab_set)
+        atab = make_int4(D.abits_of[0] ? D.abits_of[0] : 2, D.abits_of[1] ? D.abits_of[1] : 4,
+                         D.abits_of[2] ? D.abits_of[2] : 8, D.abits_of[3] ? D.abits_of[3] : 16);
+    const int32_t atab_h[4] = {atab.x, atab.y, atab.z, atab.w};
 
-    // b*_t from a_{t-1}, then per-row activation bits (W4-pinned table)
+    // b*_t from a_{t-1}, then per-row activation bits (variant table)
+    auto select = [&](cudaStream_t s_sel, bool prefill_rows) -> dyq_status_t {
+        const dyq_stream_t ss = (dyq_stream_t)s_sel;
+        if (w8) {
+            DYQ_TRY(dyq_select_bits(state, E, m->t == 0 ? nullptr : prev, bits, nullptr, nullptr, ss));
+            if (prefill_rows &&
+                launch_pdl(variant_route_kernel, dim3(1), dim3(256), 0, s_sel, (const int32_t*)bits, E, S, wtab, atab,
+                           rbp, rb8p, gates) != cudaSuccess)
+                return set_error(DYQ_ECUDA, "variant_route_kernel launch");
+            if (launch_pdl(variant_route_kernel, dim3(1), dim3(32), 0, s_sel, (const int32_t*)bits, E, 1, wtab, atab,
+                           rbd, rb8d, gates + 2) != cudaSuccess)
+                return set_error(DYQ_ECUDA, "variant_route_kernel launch");
+            return check_launch("variant_route_kernel");
+        }
+        if (prefill_rows)
+            DYQ_TRY(dyq_select_route(state, E, m->t == 0 ? nullptr : prev, bits, S, atab_set ? atab_h : nullptr, rbp,
+                                     nullptr, nullptr, ss));
+        else
+            DYQ_TRY(dyq_select_bits(state, E, m->t == 0 ? nullptr : prev, bits, nullptr, nullptr, ss));
+        return dyq_route_bits(bits, E, 1, atab_set ? atab_h : nullptr, rbd, ss);
+    };
     if (forced) {
         DYQ_TRY(dyq_route_bits(forced, E, S, nullptr, rbp, stream));
         DYQ_TRY(dyq_route_bits(forced, E, 1, nullptr, rbd, stream));
         bits = const_cast<int32_t*>(forced);  // detok copies it to bits_out
+    } else if (paper) {
+        // the selector overlaps the visual prefill on a side stream
+        // (fork / join by events: one graph with two branches under capture);
+        // the prefill runs at the fixed prefill width on the W4 copy
+        if (cudaEventRecord(m->ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(m->side, m->ev_fork, 0) != cudaSuccess)
+            return check_launch("paper-mode fork");
+        DYQ_TRY(select(m->side, false));
+        if (cudaEventRecord(m->ev_join, m->side) != cudaSuccess) return check_launch("paper-mode join record");
+        if (launch_pdl(fill_i32_kernel, dim3((MP + 255) / 256), dim3(256), 0, st, rbp, MP, pre_bits) != cudaSuccess)
+            return set_error(DYQ_ECUDA, "fill_i32_kernel launch");
+        DYQ_TRY(check_launch("fill_i32_kernel"));
     } else {
-        DYQ_TRY(dyq_select_route(state, E, m->t == 0 ? nullptr : prev, bits, S, nullptr, rbp, nullptr, nullptr,
-                                 stream));
-        DYQ_TRY(dyq_route_bits(bits, E, 1, nullptr, rbd, stream));
+        DYQ_TRY(select(st, true));
     }
 
-    auto layer = [&](int l, int M, int32_t* rb, bool prefill, int pos) -> dyq_status_t {
+    // one qlinear of the block: on the W4 copy with rows rb, and (variant
+    // table) on the W8 copy with rows rb8, each gated on having live rows
+    auto qlin = [&](int which, size_t li, const uint16_t* x, int M, int32_t* rb, int32_t* rb8, const int32_t* g,
+                    uint16_t* y, bool gated_in) -> dyq_status_t {
+        const bool two = w8 && rb8 != nullptr;
+        if (two) g_gate = g;
+        rc = gated_in ? qlinear_gated(&wd[which], m->codes[li + which], m->meta[li + which], x, M, rb, 0, y, 1,
+                                      ws[which], L.ws_bytes[which], err, st)
+                      : dyq_qlinear(&wd[which], m->codes[li + which], m->meta[li + which], x, M, rb, 0, y, 1,
+                                    ws[which], L.ws_bytes[which], err, stream);
+        if (two && !rc) {
+            g_gate = g + 1;
+            rc = gated_in ? qlinear_gated(&wd[4 + which], m->codes8[li + which], m->meta8[li + which], x, M, rb8, 0, y,
+                                          1, ws8[which], L.ws_bytes[4 + which], err, st)
+                          : dyq_qlinear(&wd[4 + which], m->codes8[li + which], m->meta8[li + which], x, M, rb8, 0, y,
+                                        1, ws8[which], L.ws_bytes[4 + which], err, stream);
+        }
+        g_gate = nullptr;
+        return rc;
+    };
+
+    auto layer = [&](int l, int M, int32_t* rb, int32_t* rb8, const int32_t* g, bool prefill, int pos)
+        -> dyq_status_t {
         const size_t li = (size_t)4 * l;
-        DYQ_TRY(dyq_qlinear(&wd[0], m->codes[li], m->meta[li], xn, M, rb, 0, qkv, 1, ws[0], L.ws_bytes[0], err,
-                            stream));
+        DYQ_TRY(qlin(0, li, xn, M, rb, rb8, g, qkv, false));
         DYQ_TRY(dyq_rope(qkv, M, prefill ? S : 1, prefill ? 0 : pos, d, H, D.rope_theta, stream));
         if (prefill)
             DYQ_TRY(dyq_attention_prefill(qkv, E, S, d, H, kv, l, NL, L.T, att, stream));
         else
             DYQ_TRY(dyq_attention_decode(qkv, E, pos, d, H, kv, l, NL, L.T, att, stream));
-        DYQ_TRY(dyq_qlinear(&wd[1], m->codes[li + 1], m->meta[li + 1], att, M, rb, 0, delta, 1, ws[1], L.ws_bytes[1],
-                            err, stream));
+        DYQ_TRY(qlin(1, li, att, M, rb, rb8, g, delta, false));
         DYQ_TRY(dyq_add_rmsnorm(h, delta, D.mlp_norm + (size_t)l * d, M, d, D.rms_eps, xn, stream));
-        DYQ_TRY(dyq_qlinear(&wd[2], m->codes[li + 2], m->meta[li + 2], xn, M, rb, 0, gu, 1, ws[2], L.ws_bytes[2],
-                            err, stream));
+        DYQ_TRY(qlin(2, li, xn, M, rb, rb8, g, gu, false));
         // SwiGLU fused into the down projection's activation quantization
         // (bit-identical to dyq_silu_mul + dyq_qlinear; one launch less per layer)
-        DYQ_TRY(qlinear_gated(&wd[3], m->codes[li + 3], m->meta[li + 3], gu, M, rb, 0, delta, 1, ws[3], L.ws_bytes[3],
-                              err, st));
+        DYQ_TRY(qlin(3, li, gu, M, rb, rb8, g, delta, true));
         const uint16_t* nw = l + 1 < NL ? D.attn_norm + (size_t)(l + 1) * d : D.final_norm;
         DYQ_TRY(dyq_add_rmsnorm(h, delta, nw, M, d, D.rms_eps, xn, stream));
         return DYQ_OK;
@@ -1081,7 +1228,8 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
         return set_error(DYQ_ECUDA, "embed_prefill_kernel launch");
     DYQ_TRY(check_launch("embed_prefill_kernel"));
     DYQ_TRY(dyq_add_rmsnorm(h, nullptr, D.attn_norm, MP, d, D.rms_eps, xn, stream));
-    for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, MP, rbp, true, 0));
+    for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, MP, rbp, paper ? nullptr : rb8p, gates, true, 0));
+    if (paper && cudaStreamWaitEvent(st, m->ev_join, 0) != cudaSuccess) return check_launch("paper-mode join");
     DYQ_TRY(dyq_head_argmax(xn + (size_t)(S - 1) * d, E, S, d, D.head_bins, D.n_bins, logits, tok, D.n_act, stream));
     // ---- decode passes: one action token per pass
     for (int t = 1; t < D.n_act; ++t) {
@@ -1090,7 +1238,7 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
             return set_error(DYQ_ECUDA, "embed_action_kernel launch");
         DYQ_TRY(check_launch("embed_action_kernel"));
         DYQ_TRY(dyq_add_rmsnorm(h, nullptr, D.attn_norm, E, d, D.rms_eps, xn, stream));
-        for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, E, rbd, false, S + t - 1));
+        for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, E, rbd, rb8d, gates + 2, false, S + t - 1));
         DYQ_TRY(dyq_head_argmax(xn, E, 1, d, D.head_bins, D.n_bins, logits, tok + t, D.n_act, stream));
     }
     if (launch_pdl(detok_kernel, dim3((E * D.n_act + 127) / 128), dim3(128), 0, st, tok, E, D.n_act, D.n_bins,

@@ -95,6 +95,7 @@ struct PreArgs {
     TpPeers tp;          // fused TP epilogue (TP instantiation only; one whole unit per CTA)
     float* part;         // stream-K partial tiles [2 * gridDim.x][144 tokens][128 rows] fp32
     int* cnt;            // [gridDim.x] per-reducer arrival counters (zeroed once, self-resetting)
+    const int32_t* gate; // dyq_qlinear_masked gate or null
     uint64_t* trace;     // dyq_trace_enable buffer or null (kernel id 2; events below)
     uint32_t serial;
 };
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
     const uint8_t* mode = a.act + a.P.mode_off;  // per token tile: 1 = e4m3 operands (written by the quantizer)
 
     extern __shared__ __align__(1024) uint8_t smem[];
+    if (gate_closed(a.gate)) return;
     if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 2, 0);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
@@ -500,7 +502,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                         for (int ii = 0; ii < NB * 8; ++ii) {
                             const int blk = ii >> 3, si = (ii >> 2) & 1, j = ii & 3;
                             const int dr = 16 * si + 8 * (j >> 1), dm = blk * 8 + (j & 1);
-                            if (rb + dr < nsub * 16 && mb + dm < a.M)
+                            if (rb + dr < nsub * 16 && mb + dm < a.M && !(a.row_bits && a.row_bits[mb + dm] == 0))
                                 reinterpret_cast<float*>(a.y)[(size_t)(mb + dm) * L.N + n0 + dr] = facc[ii];
                             facc[ii] = 0.f;
                         }
@@ -521,6 +523,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                         const int c = k >> 4, part = k & 15;
                         const int m = tt * PT + c;
                         if (part >= 2 * nsub || m >= a.M) continue;
+                        if (a.row_bits && a.row_bits[m] == 0) continue;  // masked row: y untouched
                         const uint4 v = *reinterpret_cast<const uint4*>(stg + c * STG_ROW + part * 16);
                         if constexpr (TP) {  // bf16 into every rank's full y, this rank's columns
                             const size_t o = ((size_t)m * a.tp.ldy + a.tp.col0 + (size_t)tile * 128) * 2 + part * 16;
@@ -614,7 +617,8 @@ template <int KH>  // inputs per thread = G / 2
 __global__ void __launch_bounds__(2 * PT) actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
                                                           const int32_t* __restrict__ row_bits, int bits,
                                                           uint8_t* __restrict__ act, PreActLayout P, int64_t* err,
-                                                          int e4m3_ok, int gated) {
+                                                          int e4m3_ok, int gated, const int32_t* gate) {
+    if (gate_closed(gate)) return;
     ptx::pdl_wait();  // x / row_bits come from the preceding kernels
     ptx::pdl_launch_dependents();
     const int NG = L.NG, G = L.G;
@@ -764,7 +768,7 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, L.G == 64 ? actquant_pre_kernel<32> : actquant_pre_kernel<64>, L, x, M, row_bits, bits,
-                                             reinterpret_cast<uint8_t*>(act), P, err, pre_e4m3_enabled(L) ? 1 : 0, gated);
+                                             reinterpret_cast<uint8_t*>(act), P, err, pre_e4m3_enabled(L) ? 1 : 0, gated, g_gate);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "actquant_pre_kernel launch: %s", cudaGetErrorString(e));
     return check_launch("actquant_pre_kernel");
 }
@@ -888,6 +892,7 @@ dyq_status_t launch_prefill(const WLayout& L, const void* codes, const void* met
     a.cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(const_cast<void*>(act)) - PRE_CNT_BYTES);
     a.trace = g_trace;
     a.serial = g_trace_serial++;
+    a.gate = g_gate;
     const cudaError_t e = I_out ? pre_dispatch<true>(a, grid, st)
                           : tp  ? pre_dispatch<false, true>(a, grid, st)
                                 : pre_dispatch<false>(a, grid, st);

@@ -23,6 +23,7 @@ _SIGS = {
     "dyq_version": [],
     "dyq_error_reset": [P, P],
     "dyq_error_read": [P, P, P],
+    "dyq_check_error": [P, P, P],
     "dyq_pack_weights_size": [P, P, P],
     "dyq_pack_weights": [P, P, P, P, P, P],
     "dyq_unpack_for_check": [P, P, P, P, P, P, P],
@@ -36,6 +37,7 @@ _SIGS = {
     "dyq_qlinear_plan": [P, i32, P, P],
     "dyq_workspace_init": [P, sz, P],
     "dyq_qlinear": [P, P, P, P, i32, P, i32, P, i32, P, sz, P, P],
+    "dyq_qlinear_masked": [P, P, P, P, i32, P, P, P, i32, P, sz, P, P],
     "dyq_qlinear_i32_partials": [P, P, P, P, i32, P, i32, P, P, sz, P, P],
     "dyq_act_quant_for_check": [P, P, i32, P, i32, P, P, P, P, P, sz, P, P],
     "dyq_set_path": [i32],
@@ -178,6 +180,18 @@ def error_reset(err, stream=None):
     _call("dyq_error_reset", _ptr(err), _stream(stream))
 
 
+def check_error(err, stream=None):
+    """Non-blocking poll: None while the copy is in flight, else the recorded
+    index (-1 = none) -- raises nothing; DYQ_ENONFINITE is reported as the index."""
+    out = C.c_int64(0)
+    rc = lib().dyq_check_error(_ptr(err), C.byref(out), _stream(stream))
+    if rc not in (0, 4):
+        raise DyqError(rc, "dyq_check_error", lib().dyq_last_error().decode())
+    if out.value == -1 and rc == 0:
+        return None
+    return -1 if out.value == (1 << 63) - 1 else out.value
+
+
 def error_read(err, stream=None) -> int:
     """Returns the first non-finite element index or -1."""
     out = C.c_int64(0)
@@ -268,6 +282,12 @@ def act_quant(wd: WDesc, x, M: int, row_bits, bits: int, ws, err=None, stream=No
           ws.numel() * ws.element_size(), _ptr(err), _stream(stream))
 
 
+def qlinear_masked(wd: WDesc, codes, meta, x, M: int, row_bits, gate, y, y_dtype: int, ws, err=None, stream=None):
+    """dyq_qlinear_masked: rows with row_bits 0 untouched; *gate == 0 -> no-op."""
+    _call("dyq_qlinear_masked", C.byref(wd), _ptr(codes), _ptr(meta), _ptr(x), M, _ptr(row_bits), _ptr(gate),
+          _ptr(y), y_dtype, _ptr(ws), ws.numel() * ws.element_size(), _ptr(err), _stream(stream))
+
+
 def qlinear_q(wd: WDesc, codes, meta, x, M: int, row_bits, bits: int, y, y_dtype: int, ws,
               stream=None):
     _call("dyq_qlinear_q", C.byref(wd), _ptr(codes), _ptr(meta), _ptr(x), M, _ptr(row_bits), bits,
@@ -341,7 +361,10 @@ class ModelDesc(C.Structure):
                 ("rms_eps", C.c_float), ("rope_theta", C.c_float),
                 ("codes", C.POINTER(C.c_void_p)), ("meta", C.POINTER(C.c_void_p)),
                 ("attn_norm", C.c_void_p), ("mlp_norm", C.c_void_p), ("final_norm", C.c_void_p),
-                ("embed", C.c_void_p), ("head_bins", C.c_void_p), ("kv", C.c_void_p), ("scratch", C.c_void_p)]
+                ("embed", C.c_void_p), ("head_bins", C.c_void_p), ("kv", C.c_void_p), ("scratch", C.c_void_p),
+                ("codes_w8", C.POINTER(C.c_void_p)), ("meta_w8", C.POINTER(C.c_void_p)),
+                ("wbits_of", C.c_int32 * 4), ("abits_of", C.c_int32 * 4),
+                ("paper_mode", C.c_int32), ("prefill_bits", C.c_int32)]
 
 
 def add_rmsnorm(h, delta, w, M: int, d: int, eps: float, y, stream=None):
@@ -381,7 +404,11 @@ class Model:
 
     def __init__(self, layers, attn_norm, mlp_norm, final_norm, embed, head_bins, E: int,
                  n_heads: int = 32, n_vis: int = 256, n_text: int = 32, n_act: int = 7,
-                 rms_eps: float = 1e-5, rope_theta: float = 10000.0, stream=None):
+                 rms_eps: float = 1e-5, rope_theta: float = 10000.0, stream=None,
+                 layers_w8=None, wbits_of=None, abits_of=None, paper_mode: int = 0, prefill_bits: int = 0):
+        """layers_w8: optional W8 copies (same structure) for the variant table
+        wbits_of / abits_of (per b* in 2, 4, 8, 16); paper_mode: b* selected on
+        a side stream overlapping the prefill, which runs at prefill_bits."""
         import torch
         qkv0 = layers[0][0].wd
         d = qkv0.K
@@ -395,6 +422,18 @@ class Model:
                               C.cast(self._codes, C.POINTER(C.c_void_p)), C.cast(self._meta, C.POINTER(C.c_void_p)),
                               attn_norm.data_ptr(), mlp_norm.data_ptr(), final_norm.data_ptr(), embed.data_ptr(),
                               head_bins.data_ptr(), None, None)
+        if layers_w8 is not None:
+            self._keep.append(layers_w8)
+            self._codes8 = (C.c_void_p * (4 * nl))(*[l.codes.data_ptr() for L in layers_w8 for l in L])
+            self._meta8 = (C.c_void_p * (4 * nl))(*[l.meta.data_ptr() for L in layers_w8 for l in L])
+            self.desc.codes_w8 = C.cast(self._codes8, C.POINTER(C.c_void_p))
+            self.desc.meta_w8 = C.cast(self._meta8, C.POINTER(C.c_void_p))
+        if wbits_of is not None:
+            self.desc.wbits_of = (C.c_int32 * 4)(*wbits_of)
+        if abits_of is not None:
+            self.desc.abits_of = (C.c_int32 * 4)(*abits_of)
+        self.desc.paper_mode = paper_mode
+        self.desc.prefill_bits = prefill_bits
         kvb, scb = C.c_size_t(0), C.c_size_t(0)
         _call("dyq_model_size", C.byref(self.desc), C.byref(kvb), C.byref(scb))
         dev = embed.device

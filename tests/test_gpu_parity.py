@@ -205,6 +205,13 @@ def test_nonfinite_reported_with_index():
     dyq.error_reset(err)
     y = torch.zeros(M, N, dtype=torch.float32, device=DEV)
     dyq.qlinear(wd, codes, meta, t_u16(x), M, None, 8, y, 0, ws, err)
+    # non-blocking poll (dyq_check_error): None while the copy is in flight
+    import time
+    t0 = time.time()
+    got = dyq.check_error(err)
+    while got is None and time.time() - t0 < 10:
+        got = dyq.check_error(err)
+    assert got == 2 * K + 131
     assert dyq.error_read(err) == 2 * K + 131
     # weights too
     w2 = w.copy()
