@@ -96,7 +96,7 @@ struct PreArgs {
     float* part;         // stream-K partial tiles [2 * gridDim.x][144 tokens][128 rows] fp32
     int* cnt;            // [gridDim.x] per-reducer arrival counters (zeroed once, self-resetting)
     const int32_t* gate; // dyq_qlinear_masked gate or null
-    uint64_t* trace;     // dyq_trace_enable buffer or null (kernel id 2; events below)
+    uint64_t* trace;     // dyq_trace_enable buffer or null (kernel id 4; events below)
     uint32_t serial;
 };
 // trace events (tools/trace_prefill.py): 0 CTA entry, 1 promotion past
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 
     extern __shared__ __align__(1024) uint8_t smem[];
     if (gate_closed(a.gate)) return;
-    if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 2, 0);
+    if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 4, 0);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;   // [2]
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
         // segment's K-groups; the epilogue runs once per segment.
         ptx::pdl_wait();
         const bool tr0 = a.trace && threadIdx.x == PR_WARP0 * 32;
-        if (tr0) trace_ev(a.trace, a.serial, 2, 1);
+        if (tr0) trace_ev(a.trace, a.serial, 4, 1);
         const int e = warp - PR_WARP0;  // 0..7
         const int q = warp & 3;         // TMEM lane quadrant (hardware: warp id % 4)
         const int h = e >> 2;           // column half: tokens [72h, 72h + 72)
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             for (int g = g0; g < g1; ++g, ++i) {
                 const int b = i & 1;
                 ptx::mbar_wait(&tfull[b], (i >> 1) & 1);
-                if (tr0 && i == 0) trace_ev(a.trace, a.serial, 2, 2);
+                if (tr0 && i == 0) trace_ev(a.trace, a.serial, 4, 2);
                 tc::fence_after();
                 const uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
                 const float* swp = reinterpret_cast<const float*>(st + a.off_meta) + swo;
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 if (lane == 0) ptx::mbar_arrive(&empty[s]);
                 if (++s == S) s = 0;
             }
-            if (tr0) trace_ev(a.trace, a.serial, 2, 3);
+            if (tr0) trace_ev(a.trace, a.serial, 4, 3);
             if constexpr (!PARTIALS) {
                 // ---- segment end.  whole unit: y directly; otherwise an fp32
                 // partial tile [144 tokens][128 rows] for prefill_fixup_kernel
@@ -587,13 +587,13 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                     write_out();
                 }
             }
-            if (tr0) trace_ev(a.trace, a.serial, 2, 4);
+            if (tr0) trace_ev(a.trace, a.serial, 4, 4);
             w += g1 - g0;
         }
     }
     tc::fence_before();
     __syncthreads();
-    if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 2, 5);
+    if (threadIdx.x == 0) trace_ev(a.trace, a.serial, 4, 5);
     if (warp == 1) {
         tc::fence_after();
         tc::dealloc(tmem, 512);

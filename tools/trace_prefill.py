@@ -1,5 +1,5 @@
 """Per-CTA timeline of the persistent prefill kernel from the %globaltimer
-trace (dyq_trace_enable, kernel id 2).  Runs R back-to-back qlinear calls of
+trace (dyq_trace_enable, kernel id 4).  Runs R back-to-back qlinear calls of
 one Llama linear (act-quant + prefill, as in the block step) inside a CUDA
 graph with tracing on, then prints per prefill launch (relative to the first
 CTA entry of that launch, us): CTA entry spread, promotion past
@@ -53,7 +53,7 @@ serial = (tag >> 32).astype(np.int64)
 kern = ((tag >> 24) & 0xff).astype(np.int64)
 ev = ((tag >> 16) & 0xff).astype(np.int64)
 cta = (tag & 0xffff).astype(np.int64)
-sel = kern == 2
+sel = kern == 4
 t0g = ns[sel].min() if sel.any() else 0
 prev_end = None
 for sr in sorted(set(serial[sel].tolist())):
