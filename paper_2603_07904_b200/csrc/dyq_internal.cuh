@@ -112,8 +112,9 @@ __device__ __forceinline__ bool dec_call_centred(int M, int m0, const int32_t* r
     return c;
 }
 
-// Prefill activation operand (M > 16): per (144-token tile, K-group) the UMMA
-// canonical K-major no-swizzle B operand of the tcgen05 kernel,
+// Prefill activation operand (M > 16): per (144-token tile, K-group) one
+// record [s_x | B] (one bulk copy per group) holding the UMMA canonical
+// K-major no-swizzle B operand of the tcgen05 kernel,
 //   x16 [TT][NG][G/16 K-steps][144 rows] bf16: centred codes Xq - z_x (exact),
 //       x for A16 rows, 0 for absent rows
 //   par [TT][NG][144] f32 s_x (1 for A16 rows, 0 for absent rows)
@@ -122,7 +123,7 @@ __device__ __forceinline__ bool dec_call_centred(int M, int m0, const int32_t* r
 constexpr size_t PRE_CNT_BYTES = 1024;  // prefill stream-K counters, just before the prefill area
 struct PreActLayout {
     size_t codes_off, x16_off, par_off, mode_off, bytes;
-    size_t codes_group, x16_group;
+    size_t codes_group, x16_group, rec;
 };
 
 // ---------------------------------------------------------------- tracing

@@ -70,6 +70,12 @@ constexpr int PAR_BYTES = PT * 4;  // per (tile, group): float s_x[144] (1 for A
 constexpr int XF_WARP0 = 3, XF_WARPS = 4;
 constexpr int PR_WARP0 = 7, PR_WARPS = 8;  // promotion warps
 constexpr int STG_ROW = 128 * 2 + 16;  // epilogue staging: bytes per token (128 bf16 rows + pad)
+#ifndef DYQ_PRE_EXP
+// timing-only experiments (tools/build_variant.py; results are wrong): bit 0
+// promotion without its math, 1 transform without its work, 2 no MMAs (commit
+// only), 3 promotion without TMEM loads.  0 in product builds.
+#define DYQ_PRE_EXP 0
+#endif
 #ifndef DYQ_PRE_MIN_GROUPS
 #define DYQ_PRE_MIN_GROUPS 16  // stream-K: at least this many K-groups per CTA
 #endif
@@ -217,9 +223,9 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 const uint32_t bbytes = mode[k.tt] ? KSTEPS * BSTEP / 2 : KSTEPS * BSTEP;  // e4m3: K = 32 per step
                 uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
                 const size_t tg = (size_t)k.tt * NG + k.g;
-                ptx::mbar_arrive_expect_tx(&full[s], bbytes + PAR_BYTES);
-                ptx::bulk_g2s(st + a.off_b, a.act + a.P.x16_off + tg * a.P.x16_group, bbytes, &full[s]);
-                ptx::bulk_g2s(st + a.off_par, a.act + a.P.par_off + tg * PAR_BYTES, PAR_BYTES, &full[s]);
+                // one copy per group: the record is [s_x | B operand] (stage: off_b = off_par + PAR_BYTES)
+                ptx::mbar_arrive_expect_tx(&full[s], PAR_BYTES + bbytes);
+                ptx::bulk_g2s(st + a.off_par, a.act + tg * a.P.rec, PAR_BYTES + bbytes, &full[s]);
                 if (++s == S) { s = 0; ph ^= 1; }
             }
         }
@@ -238,7 +244,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             ptx::mbar_wait(&afull[ai], aph);   // A operand written to TMEM
             if (i >= 2) ptx::mbar_wait(&tempty[b], ((i >> 1) - 1) & 1);
             tc::fence_after();
-            if (lane == 0) {
+            if (lane == 0 && !(DYQ_PRE_EXP & 4)) {
                 const uint32_t st = sbase + s * a.stage_bytes;
                 const uint32_t d = tmem + b * PT;
                 const uint32_t at = tmem + ACC_COLS + ai * A_COLS;
@@ -255,6 +261,10 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                         tc::mma_f16_ta(d, at + ks * 8, bd, idesc, ks > 0);
                     }
                 }
+                tc::commit(ptx::smem_u32(&tfull[b]));
+                tc::commit(ptx::smem_u32(&empty[s]));
+                tc::commit(ptx::smem_u32(&aempty[ai]));
+            } else if (lane == 0) {
                 tc::commit(ptx::smem_u32(&tfull[b]));
                 tc::commit(ptx::smem_u32(&empty[s]));
                 tc::commit(ptx::smem_u32(&aempty[ai]));
@@ -287,7 +297,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 #pragma unroll
             for (int si = 0; si < 2; ++si) {
                 const int sub = 2 * q + si;
-                if (sub >= nsub) break;
+                if (sub >= nsub || (DYQ_PRE_EXP & 2)) break;
                 const uint32_t tl = at + ((uint32_t)(32 * q + 16 * si) << 16);
                 // zero points of rows gid and gid+8 are adjacent metadata slots
                 const uint32_t z01 = *reinterpret_cast<const uint16_t*>(zrow + sub * 16 + 2 * (lane >> 2));
@@ -459,6 +469,11 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                                 }
                             }
                 };
+                if (DYQ_PRE_EXP & 8) {
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[b]);
+                } else {
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {  // blocks 0-3, 4-7
                     uint32_t v[32];
@@ -466,7 +481,8 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                     tc::ld16x256_x4(tb + (16u << 16) + c * 32, v + 16);
                     tc::wait_ld();
                     if (PARTIALS) partials(v, 4, c * 4);
-                    else promote(v, 4, c * 4);
+                    else if (!(DYQ_PRE_EXP & 1)) promote(v, 4, c * 4);
+                    else facc[c] += __uint_as_float(v[c]);
                 }
                 {  // block 8
                     uint32_t v[8];
@@ -477,7 +493,9 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&tempty[b]);
                     if (PARTIALS) partials(v, 1, 8);
-                    else promote(v, 1, 8);
+                    else if (!(DYQ_PRE_EXP & 1)) promote(v, 1, 8);
+                    else facc[2] += __uint_as_float(v[2]);
+                }
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&empty[s]);
@@ -630,7 +648,7 @@ __global__ void __launch_bounds__(2 * PT) actquant_pre_kernel(WLayout L, const u
     const bool f8 = e4m3_ok && __syncthreads_and(m >= M || b == 2 || b == 4);
     const size_t tg = (size_t)tt * NG + g;
     if (threadIdx.x == 0 && g == 0) act[P.mode_off + tt] = f8 ? 1 : 0;  // read by the MMA kernel
-    uint8_t* xg = act + P.x16_off + tg * P.x16_group;
+    uint8_t* xg = act + tg * P.rec + PAR_BYTES;  // record [s_x | B]
     const int k0 = half * KH;  // inputs k0 .. k0 + KH - 1
     const uint16_t* src = x + (size_t)(m < M ? m : 0) * L.K * (gated ? 2 : 1) + (size_t)g * G + k0;  // gated: [g | u]
     constexpr int NW = KH / 2;  // 32-bit words per thread
@@ -671,7 +689,7 @@ __global__ void __launch_bounds__(2 * PT) actquant_pre_kernel(WLayout L, const u
     vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, 1));
     bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, 1));
     if (bad != 0x7fffffff && half == 0) report_nonfinite(err, (int64_t)m * L.K + (int64_t)g * G + bad);
-    float* sxo = reinterpret_cast<float*>(act + P.par_off + tg * PAR_BYTES) + row;
+    float* sxo = reinterpret_cast<float*>(act + tg * P.rec) + row;
     const bool quant = b == 2 || b == 4 || b == 8;
     float s = 1.f;
     int z = 0;
@@ -746,10 +764,11 @@ PreActLayout pre_act_layout(const WLayout& L, int M) {
     const int TT = (M + PT - 1) / PT;
     P.codes_group = 0;
     P.codes_off = 0;
-    P.x16_group = (size_t)(L.G / 16) * PT * 32;
-    P.x16_off = 0;
-    P.par_off = ((size_t)TT * L.NG * P.x16_group + 255) & ~(size_t)255;
-    P.mode_off = P.par_off + (((size_t)TT * L.NG * PAR_BYTES + 255) & ~(size_t)255);
+    P.x16_group = (size_t)(L.G / 16) * PT * 32;  // B operand bytes per (tile, group)
+    P.rec = PAR_BYTES + P.x16_group;             // record [s_x (144 f32) | B]
+    P.x16_off = PAR_BYTES;
+    P.par_off = 0;
+    P.mode_off = ((size_t)TT * L.NG * P.rec + 255) & ~(size_t)255;
     P.bytes = P.mode_off + (((size_t)TT + 255) & ~(size_t)255);
     return P;
 }
@@ -830,9 +849,9 @@ static cudaError_t pre_launch(const PreArgs& a0, int grid, cudaStream_t st) {
     const int raw = SPG * 8 * 512 * (WBITS / 4);
     const int bbytes = (G / 16) * PT * 32;
     a.off_meta = raw;
-    a.off_b = (a.off_meta + META_BLOCK + 127) & ~127;
-    a.off_par = a.off_b + bbytes;
-    a.stage_bytes = (a.off_par + PAR_BYTES + 127) & ~127;
+    a.off_par = (a.off_meta + META_BLOCK + 127) & ~127;
+    a.off_b = a.off_par + PAR_BYTES;  // 16-B aligned (canonical no-swizzle layout)
+    a.stage_bytes = (a.off_b + bbytes + 127) & ~127;
     constexpr int stg_bytes = PT * STG_ROW;
     a.stages = (226 * 1024 - 1024 - stg_bytes) / a.stage_bytes;
     if (a.stages > DYQ_PRE_MAX_STAGES) a.stages = DYQ_PRE_MAX_STAGES;
