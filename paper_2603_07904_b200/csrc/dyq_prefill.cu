@@ -76,10 +76,25 @@ constexpr int STG_ROW = 128 * 2 + 16;  // epilogue staging: bytes per token (128
 // only), 3 promotion without TMEM loads.  0 in product builds.
 #define DYQ_PRE_EXP 0
 #endif
+#ifndef DYQ_PRE_GTRACE
+// per-group %globaltimer stamps of CTA 0 into the trace buffer (timing-only
+// builds, tools/trace_prefill_groups.py): slot 16 + 512 * event + group
+#define DYQ_PRE_GTRACE 0
+#endif
 #ifndef DYQ_PRE_MIN_GROUPS
 #define DYQ_PRE_MIN_GROUPS 16  // stream-K: at least this many K-groups per CTA
 #endif
 constexpr uint32_t ACC_COLS = 2 * PT;   // TMEM: two 144-column accumulators, then the A buffers
+
+__device__ __forceinline__ void gstamp(uint64_t* tr, int ev, int i) {
+#if DYQ_PRE_GTRACE
+    if (tr && blockIdx.x == 0 && i < 512) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tr[16 + 512 * ev + i] = t;
+    }
+#endif
+}
 
 struct PreArgs {
     WLayout L;
@@ -224,6 +239,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
                 const size_t tg = (size_t)k.tt * NG + k.g;
                 // one copy per group: the record is [s_x | B operand] (stage: off_b = off_par + PAR_BYTES)
+                gstamp(a.trace, 6, i);
                 ptx::mbar_arrive_expect_tx(&full[s], PAR_BYTES + bbytes);
                 ptx::bulk_g2s(st + a.off_par, a.act + tg * a.P.rec, PAR_BYTES + bbytes, &full[s]);
                 if (++s == S) { s = 0; ph ^= 1; }
@@ -241,8 +257,11 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             const int b = i & 1;
             const bool f8 = WBITS == 4 && mode[k.tt];
             ptx::mbar_wait(&full[s], ph);      // B operand landed
+            if (lane == 0) gstamp(a.trace, 0, i);
             ptx::mbar_wait(&afull[ai], aph);   // A operand written to TMEM
+            if (lane == 0) gstamp(a.trace, 1, i);
             if (i >= 2) ptx::mbar_wait(&tempty[b], ((i >> 1) - 1) & 1);
+            if (lane == 0) gstamp(a.trace, 2, i);
             tc::fence_after();
             if (lane == 0 && !(DYQ_PRE_EXP & 4)) {
                 const uint32_t st = sbase + s * a.stage_bytes;
@@ -392,6 +411,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
             if (lane == 0) {
                 ptx::mbar_arrive(&afull[ai]);
                 ptx::mbar_arrive(&empty[s]);
+                if (warp == XF_WARP0) gstamp(a.trace, 5, i);
             }
             if (++s == S) { s = 0; ph ^= 1; }
             if (++ai == NA) { ai = 0; aph ^= 1; }
@@ -429,6 +449,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 const int b = i & 1;
                 ptx::mbar_wait(&tfull[b], (i >> 1) & 1);
                 if (tr0 && i == 0) trace_ev(a.trace, a.serial, 4, 2);
+                if (threadIdx.x == PR_WARP0 * 32) gstamp(a.trace, 3, i);
                 tc::fence_after();
                 const uint8_t* st = stage0 + (size_t)s * a.stage_bytes;
                 const float* swp = reinterpret_cast<const float*>(st + a.off_meta) + swo;
@@ -499,6 +520,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&empty[s]);
+                if (threadIdx.x == PR_WARP0 * 32) gstamp(a.trace, 4, i);
                 if (++s == S) s = 0;
             }
             if (tr0) trace_ev(a.trace, a.serial, 4, 3);
