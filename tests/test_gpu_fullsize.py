@@ -1,7 +1,8 @@
 """Full-size parity in bench.py's launch configuration (BASELINE configs[1] /
 configs[2]): every Llama-2-7B block linear (synth.LLAMA_BLOCK_LINEARS) at
 M = 8 action tokens (decode kernel) and M = 288 vision + text tokens (tcgen05
-prefill kernel), W4 G64, per-row activation bits routed as in the bench,
+prefill kernel), W4 G64 (and the W8 copy and G = 128 the bench also
+reports), per-row activation bits routed as in the bench,
 through dyq_qlinear (bf16 out, as timed; fp32 out for the tight bound) and,
 at decode, dyq_qlinear_i32_partials.
 
@@ -44,11 +45,16 @@ def _rowbits(M, mode):
     return np.full(M, mode, np.int32)
 
 
+# (wbits, group): the bench's W4 G64, the optional W8 copy and G = 128
+WG = [(4, 64), (8, 64), (4, 128)]
+CASES = [(wb, g, mode) for wb, g in WG for mode in ([2, 4, 8, 16, "mixed"] if (wb, g) == (4, 64) else [4, 16, "mixed"])]
+
+
 @pytest.mark.parametrize("name,N,K", synth.LLAMA_BLOCK_LINEARS, ids=[n for n, _, _ in synth.LLAMA_BLOCK_LINEARS])
 @pytest.mark.parametrize("M", [8, 288])
-@pytest.mark.parametrize("mode", [2, 4, 8, 16, "mixed"])
-def test_block_linear_fullsize_sampled(name, N, K, M, mode):
-    seed = zlib.crc32(f"{name}/{M}/{mode}".encode()) % 1000
+@pytest.mark.parametrize("WB,G,mode", CASES, ids=[f"W{wb}G{g}-{m}" for wb, g, m in CASES])
+def test_block_linear_fullsize_sampled(name, N, K, M, WB, G, mode):
+    seed = zlib.crc32(f"{name}/{M}/{mode}/{WB}/{G}".encode()) % 1000
     w = synth.weights_bf16_torch(N, K, seed=1 + seed, device=DEV)
     x = synth.activations_bf16_torch(M, K, seed=1000 + seed, device=DEV)
     lin = dyq.PackedLinear.from_bf16(w, group=G, wbits=WB)
@@ -72,7 +78,7 @@ def test_block_linear_fullsize_sampled(name, N, K, M, mode):
     # path is bit-checked as well
     path, ks = dyq.qlinear_plan(lin.wd, M)
     assert path == (1 if M <= 16 else 2)
-    if M == 288 and name in ("o", "down"):
+    if M == 288 and name in ("o", "down") and G == 64:
         assert ks > 1, "split-K prefill expected at this shape"
     I = torch.zeros(M, N, K // G, dtype=torch.int32, device=DEV)
     dyq.qlinear_i32_partials(lin.wd, lin.codes, lin.meta, x, M, rbt, 0, I, ws)
