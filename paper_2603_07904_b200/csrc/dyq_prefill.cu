@@ -82,7 +82,7 @@ constexpr int STG_ROW = 128 * 2 + 16;  // epilogue staging: bytes per token (128
 #define DYQ_PRE_GTRACE 0
 #endif
 #ifndef DYQ_PRE_MIN_GROUPS
-#define DYQ_PRE_MIN_GROUPS 16  // stream-K: at least this many K-groups per CTA
+#define DYQ_PRE_MIN_GROUPS 32  // stream-K: at least this many K-groups per CTA (16 / 32 / 64: o 41.9 / 38.9 / 51.4 us)
 #endif
 constexpr uint32_t ACC_COLS = 2 * PT;   // TMEM: two 144-column accumulators, then the A buffers
 
@@ -641,20 +641,21 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 }
 
 // -------------------------------------------- prefill activation quantizer
-// One CTA per (token tile tt, K-group g); thread pair (2 row, 2 row + 1) of
-// the 288 threads quantizes token row `row` of the tile: each thread holds 32
-// of the group's G = 64 inputs (16-B loads), the pair combines min / max with
-// one shuffle, and each thread writes its K steps of the B operand in the
-// UMMA canonical K-major layout with 16-B stores
+// One CTA per (token tile tt, K-group g); four threads per token row of the
+// tile (576 threads): each holds G/4 of the group's inputs (16-B loads), the
+// quad combines min / max and the non-finite index with two shuffles, and
+// each thread writes its part of the B operand in the UMMA canonical K-major
+// layout
 //   bf16: [tt][g][K step ks][row>>3][kk>>3][row&7][kk&7]   (16 k per K step)
 //   e4m3: [tt][g][K step ks][row>>3][p>>4][row&7][p&15]    (32 k per K step,
-//         p = e4m3_kpos(k))
+//         p = e4m3_kpos(k); at G = 64 a K step spans a thread pair, which
+//         swaps two words to form whole 16-B chunks)
 // holding the centred codes Xq - z_x of Eq. (2) for integer tokens (exact in
 // bf16 / e4m3), x itself for A16 tokens and 0 for absent rows; and s_x per
-// token (1 for A16 tokens, 0 for absent rows).  G = 128: the CTA loops over
-// the two 64-k halves with the same pair split (a thread owns 64 inputs).
-template <int KH>  // inputs per thread = G / 2
-__global__ void __launch_bounds__(2 * PT) actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
+// token (1 for A16 tokens, 0 for absent rows) at the head of the record.
+constexpr int AQP_TPR = 4;  // threads per token row
+template <int KH>  // inputs per thread = G / AQP_TPR
+__global__ void __launch_bounds__(AQP_TPR * PT) actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
                                                           const int32_t* __restrict__ row_bits, int bits,
                                                           uint8_t* __restrict__ act, PreActLayout P, int64_t* err,
                                                           int e4m3_ok, int gated, const int32_t* gate) {
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(2 * PT) actquant_pre_kernel(WLayout L, const u
     ptx::pdl_launch_dependents();
     const int NG = L.NG, G = L.G;
     const int g = blockIdx.x % NG, tt = blockIdx.x / NG;
-    const int row = threadIdx.x >> 1, half = threadIdx.x & 1;
+    const int row = threadIdx.x / AQP_TPR, half = threadIdx.x % AQP_TPR;  // half: quarter of the group
     const int m = tt * PT + row;
     const int b = m < M ? (row_bits ? row_bits[m] : bits) : 0;
     // tile mode (dyq_pre_tile_e4m3): every present token of tile tt at A2 / A4
@@ -706,10 +707,13 @@ __global__ void __launch_bounds__(2 * PT) actquant_pre_kernel(WLayout L, const u
                 vmax = fmaxf(vmax, v);
             }
     }
-    // pair combine (lanes 2 row, 2 row + 1 are adjacent in the warp)
+    // quad combine (the row's four threads are adjacent lanes)
     vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, 1));
     vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, 1));
     bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, 1));
+    vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, 2));
+    vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, 2));
+    bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, 2));
     if (bad != 0x7fffffff && half == 0) report_nonfinite(err, (int64_t)m * L.K + (int64_t)g * G + bad);
     float* sxo = reinterpret_cast<float*>(act + tg * P.rec) + row;
     const bool quant = b == 2 || b == 4 || b == 8;
@@ -748,8 +752,28 @@ __global__ void __launch_bounds__(2 * PT) actquant_pre_kernel(WLayout L, const u
                 *reinterpret_cast<uint4*>(rowb + KS * (PT * 32) + kh * 128) = make_uint4(o[0], o[1], o[2], o[3]);
             }
         }
+    } else if constexpr (KH == 16) {
+        // e4m3, G = 64: a 32-k K step spans thread pair (A: k 0-15, B: 16-31);
+        // chunk 0 = [A0 B0 A1 B1], chunk 1 = [A2 B2 A3 B3] (4-byte runs of k)
+        uint32_t w[4];
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4) {
+            w[r4] = 0u;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int kt = 4 * r4 + e;
+                const uint32_t q8 = quant ? (uint32_t)e4m3_of(val(kt >> 1, kt & 1)) : 0u;  // |q - z| <= 15
+                w[r4] |= q8 << (8 * e);
+            }
+        }
+        const bool isA = (half & 1) == 0;
+        const uint32_t x0 = __shfl_xor_sync(0xffffffffu, isA ? w[2] : w[0], 1);
+        const uint32_t x1 = __shfl_xor_sync(0xffffffffu, isA ? w[3] : w[1], 1);
+        const int KS = half >> 1;
+        const uint4 o = isA ? make_uint4(w[0], x0, w[1], x1) : make_uint4(x0, w[2], x1, w[3]);
+        *reinterpret_cast<uint4*>(rowb + KS * (PT * 32) + (isA ? 0 : 128)) = o;
     } else {
-        // e4m3: one 32-k K step per thread half (G = 64), two for G = 128
+        // e4m3: one 32-k K step per thread (G = 128)
 #pragma unroll
         for (int ks = 0; ks < KH / 32; ++ks) {
 #pragma unroll
@@ -801,14 +825,14 @@ dyq_status_t launch_actquant_pre(const WLayout& L, const uint16_t* x, int M, con
     const int TT = (M + PT - 1) / PT;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(TT * L.NG));
-    cfg.blockDim = dim3(2 * PT);
+    cfg.blockDim = dim3(AQP_TPR * PT);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, L.G == 64 ? actquant_pre_kernel<32> : actquant_pre_kernel<64>, L, x, M, row_bits, bits,
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, L.G == 64 ? actquant_pre_kernel<16> : actquant_pre_kernel<32>, L, x, M, row_bits, bits,
                                              reinterpret_cast<uint8_t*>(act), P, err, pre_e4m3_enabled(L) ? 1 : 0, gated, g_gate);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "actquant_pre_kernel launch: %s", cudaGetErrorString(e));
     return check_launch("actquant_pre_kernel");
