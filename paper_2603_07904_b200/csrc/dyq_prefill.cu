@@ -323,7 +323,10 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 if (WBITS == 4 && f8) {
                     // e4m3 (q - z_w): K step = slab; TMEM column 2t <- low nibbles,
                     // 2t + 1 <- high nibbles (e4m3_kpos), rows gid / gid + 8
-                    const float zf0 = 8388608.f + (float)(z01 & 0xffu), zf1 = 8388608.f + (float)(z01 >> 8);
+                    // fp16 (1024 + q) pairs by byte permutes (0x64XX is exactly 1024 + XX),
+                    // minus fp16 (1024 + z): exact (q - z), then one cvt to e4m3x2 per pair
+                    const uint32_t zh0 = 0x64006400u | ((z01 & 0xffu) * 0x00010001u);
+                    const uint32_t zh1 = 0x64006400u | ((z01 >> 8) * 0x00010001u);
 #pragma unroll
                     for (int spi = 0; spi < SPG; ++spi) {
                         const uint4 wv = *reinterpret_cast<const uint4*>(st + ((spi * nsub + sub) * 32 + lane) * 16);
@@ -332,16 +335,15 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             const int slab = j >> 1, rs = j & 1;
-                            const float zf = rs ? zf1 : zf0;
+                            const uint32_t zz = rs ? zh1 : zh0;
 #pragma unroll
                             for (int hn = 0; hn < 2; ++hn) {
                                 const uint32_t x = hn ? (ws4[j] >> 4) & 0x0F0F0F0Fu : ws4[j] & 0x0F0F0F0Fu;
-                                float v[4];
-#pragma unroll
-                                for (int bb = 0; bb < 4; ++bb)  // (2^23 + q) - (2^23 + z): exact q - z
-                                    v[bb] = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7540u + bb)) - zf;
-                                const uint32_t p01 = __nv_cvt_float2_to_fp8x2(make_float2(v[0], v[1]), __NV_SATFINITE, __NV_E4M3);
-                                const uint32_t p23 = __nv_cvt_float2_to_fp8x2(make_float2(v[2], v[3]), __NV_SATFINITE, __NV_E4M3);
+                                const uint32_t h01 = __byte_perm(x, 0x6464u, 0x5140u), h23 = __byte_perm(x, 0x6464u, 0x5342u);
+                                const __half2 d01 = __hsub2(*reinterpret_cast<const __half2*>(&h01), *reinterpret_cast<const __half2*>(&zz));
+                                const __half2 d23 = __hsub2(*reinterpret_cast<const __half2*>(&h23), *reinterpret_cast<const __half2*>(&zz));
+                                const uint32_t p01 = __nv_cvt_halfraw2_to_fp8x2(*reinterpret_cast<const __half2_raw*>(&d01), __NV_SATFINITE, __NV_E4M3);
+                                const uint32_t p23 = __nv_cvt_halfraw2_to_fp8x2(*reinterpret_cast<const __half2_raw*>(&d23), __NV_SATFINITE, __NV_E4M3);
                                 r[slab * 4 + rs * 2 + hn] = (p01 & 0xffffu) | (p23 << 16);
                             }
                         }
@@ -412,6 +414,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
                 ptx::mbar_arrive(&afull[ai]);
                 ptx::mbar_arrive(&empty[s]);
                 if (warp == XF_WARP0) gstamp(a.trace, 5, i);
+                if (warp == XF_WARP0 + 1) gstamp(a.trace, 7, i);
             }
             if (++s == S) { s = 0; ph ^= 1; }
             if (++ai == NA) { ai = 0; aph ^= 1; }

@@ -2,7 +2,7 @@
 (build with tools/build_variant.py gtrace -DDYQ_PRE_GTRACE=1, run with
 DYQ_LIB=tools/variants/libdyq_gtrace.so).  Events per group i: 0 MMA saw
 full, 1 MMA saw afull, 2 MMA saw tempty (issues next), 3 promotion saw
-tfull, 4 promotion done, 5 transform done, 6 activation copy issued.
+tfull, 4 promotion done, 5 transform done, 6 activation copy issued, 7 transform warp 4 done.
 Prints the median interval of each stage over the steady state.
 usage: python tools/trace_prefill_groups.py [linear] [M] [bits]"""
 import os
@@ -46,5 +46,5 @@ print(f"MMA full -> afull            {d(1, 0):.3f}")
 print(f"MMA afull -> tempty          {d(2, 1):.3f}")
 print(f"MMA tempty -> promo tfull    {d(3, 2):.3f}  (MMA issue + commit + wake)")
 print(f"promo tfull -> promo done    {d(4, 3):.3f}")
-print(f"transform done -> MMA afull  {d(1, 5):.3f}")
-print(f"cadence of each stamp: " + ", ".join(f"ev{e} {np.median(np.diff(t[e, lo:hi])):.3f}" for e in range(7)))
+print(f"transform done -> MMA afull  {d(1, 5):.3f} (warp 3), {d(1, 7):.3f} (warp 4)")
+print(f"cadence of each stamp: " + ", ".join(f"ev{e} {np.median(np.diff(t[e, lo:hi])):.3f}" for e in range(8)))
