@@ -164,15 +164,20 @@ __global__ void __launch_bounds__(256) attn_prefill_kernel(const uint16_t* __res
     float* ps = qs + 8 * HD;                                                          // [8][S]
     const size_t rs = (size_t)3 * d;
     const uint16_t* base = qkv + (size_t)e * S * rs;
+    // generic path (any 2-byte alignment of qkv / kv): element-wise global
+    // accesses, 32-bit only in shared memory
     for (int idx = threadIdx.x; idx < qend * (HD / 2); idx += blockDim.x) {
         const int j = idx / (HD / 2), c = (idx % (HD / 2)) * 2;
-        const uint32_t kk = *reinterpret_cast<const uint32_t*>(base + j * rs + d + hh * HD + c);
-        const uint32_t vv = *reinterpret_cast<const uint32_t*>(base + j * rs + 2 * d + hh * HD + c);
-        *reinterpret_cast<uint32_t*>(Ks + j * AKP + c) = kk;
-        *reinterpret_cast<uint32_t*>(Vs + j * HD + c) = vv;
+        const uint16_t* kp = base + j * rs + d + hh * HD + c;
+        const uint16_t* vp = base + j * rs + 2 * d + hh * HD + c;
+        const uint16_t k0 = kp[0], k1 = kp[1], v0 = vp[0], v1 = vp[1];
+        *reinterpret_cast<uint32_t*>(Ks + j * AKP + c) = (uint32_t)k0 | ((uint32_t)k1 << 16);
+        *reinterpret_cast<uint32_t*>(Vs + j * HD + c) = (uint32_t)v0 | ((uint32_t)v1 << 16);
         if (j >= q0) {  // this block's rows go to the KV cache
-            *reinterpret_cast<uint32_t*>(kv + kv_off(e, layer, 0, j, L, T, d) + hh * HD + c) = kk;
-            *reinterpret_cast<uint32_t*>(kv + kv_off(e, layer, 1, j, L, T, d) + hh * HD + c) = vv;
+            uint16_t* kc = kv + kv_off(e, layer, 0, j, L, T, d) + hh * HD + c;
+            uint16_t* vc = kv + kv_off(e, layer, 1, j, L, T, d) + hh * HD + c;
+            kc[0] = k0; kc[1] = k1;
+            vc[0] = v0; vc[1] = v1;
         }
     }
     __syncthreads();

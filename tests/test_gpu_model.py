@@ -207,3 +207,77 @@ def test_policy_step_repeat_is_deterministic():
             seq.append(act.cpu().numpy().copy())
         outs.append(np.array(seq))
     assert np.array_equal(outs[0], outs[1])
+
+
+# ------------------------------------------------ fallback (generic) kernels
+# The glue entry points take a vectorised tensor-core / 16-B path when the
+# shapes and pointers allow it; these cases force the generic kernels
+# (add_rmsnorm_kernel, attn_prefill_kernel, attn_decode_kernel,
+# head_argmax_kernel) with shapes that are not multiples of 256 or with
+# pointers 2 bytes off a 16-B boundary, against the same references.
+def _misaligned(a_bits):
+    """int16 device view of a_bits starting 2 bytes past a 16-B boundary."""
+    flat = np.ascontiguousarray(a_bits).reshape(-1)
+    buf = torch.zeros(flat.size + 8, dtype=torch.int16, device=DEV)
+    buf[1:1 + flat.size] = torch.from_numpy(flat.view(np.int16)).to(DEV)
+    v = buf[1:1 + flat.size].view(a_bits.shape)
+    assert v.data_ptr() % 16 == 2
+    return v
+
+
+@pytest.mark.parametrize("M,d,mis", [(3, 200, False), (5, 512, True)])
+def test_add_rmsnorm_generic_kernel(M, d, mis):
+    h0, de = rnd_bits((M, d), 11), rnd_bits((M, d), 12, 0.5)
+    w = glue.to_bf16_bits(1.0 + glue.from_bf16_bits(rnd_bits(d, 13, 0.2)))
+    h = _misaligned(h0) if mis else t16(h0)
+    y = torch.empty(M, d, dtype=torch.int16, device=DEV)
+    dyq.add_rmsnorm(h, t16(de), t16(w), M, d, 1e-5, y)
+    hr = glue.bf16_round(glue.from_bf16_bits(h0) + glue.from_bf16_bits(de))
+    assert np.array_equal(f64(h), hr)
+    close_bf16(f64(y), glue.rmsnorm(hr, glue.from_bf16_bits(w), 1e-5))
+
+
+@pytest.mark.parametrize("E,S", [(1, 33), (2, 9)])
+def test_attention_prefill_generic_kernel(E, S):
+    d, H, L, T = 256, 2, 2, S + 3
+    qkv0 = rnd_bits((E * S, 3 * d), 14)
+    kv = torch.zeros(E * L * 2 * T * d, dtype=torch.int16, device=DEV)
+    out = torch.empty(E * S, d, dtype=torch.int16, device=DEV)
+    dyq.attention_prefill(_misaligned(qkv0), E, S, d, H, kv, 0, L, T, out)
+    x = glue.from_bf16_bits(qkv0)
+    kvh = kv.cpu().numpy().view(np.uint16).reshape(E, L, 2, T, d)
+    for e in range(E):
+        r = slice(e * S, (e + 1) * S)
+        close_bf16(f64(out)[r], glue.attention(x[r, :d], x[r, d:2 * d], x[r, 2 * d:], causal=True))
+        assert np.array_equal(glue.from_bf16_bits(kvh[e, 0, 0, :S]), x[r, d:2 * d])
+
+
+@pytest.mark.parametrize("E,pos", [(1, 5), (3, 40)])
+def test_attention_decode_generic_kernel(E, pos):
+    d, H, L, T = 256, 2, 1, 64
+    rng = np.random.default_rng(15)
+    kvh = glue.to_bf16_bits(rng.standard_normal((E, L, 2, T, d)))
+    kv = t16(kvh.reshape(-1))
+    qkv0 = rnd_bits((E, 3 * d), 16)
+    out = torch.empty(E, d, dtype=torch.int16, device=DEV)
+    dyq.attention_decode(_misaligned(qkv0), E, pos, d, H, kv, 0, L, T, out)
+    x = glue.from_bf16_bits(qkv0)
+    for e in range(E):
+        K = glue.from_bf16_bits(kvh[e, 0, 0, :pos + 1]).copy()
+        V = glue.from_bf16_bits(kvh[e, 0, 1, :pos + 1]).copy()
+        K[pos], V[pos] = x[e, d:2 * d], x[e, 2 * d:]
+        close_bf16(f64(out)[e:e + 1], glue.attention(x[e:e + 1, :d], K, V, causal=False))
+
+
+@pytest.mark.parametrize("d,with_logits", [(264, True), (512, False)])
+def test_head_argmax_generic_kernel(d, with_logits):
+    E, nb, stride = 3, 256, 2
+    x0 = rnd_bits((E * stride, d), 17)
+    W0 = rnd_bits((nb, d), 18, 0.5)
+    logits = torch.empty(E, nb, dtype=torch.float32, device=DEV) if with_logits else None
+    tok = torch.full((E * 7,), -1, dtype=torch.int32, device=DEV)
+    dyq.head_argmax(t16(x0), E, stride, d, t16(W0), nb, logits, tok, 7)
+    lg, am = glue.head_argmax(glue.from_bf16_bits(x0)[::stride], glue.from_bf16_bits(W0))
+    if with_logits:
+        assert np.allclose(logits.cpu().numpy(), lg, rtol=1e-4, atol=1e-3)
+    assert np.array_equal(tok.cpu().numpy()[::7][:E], am)
