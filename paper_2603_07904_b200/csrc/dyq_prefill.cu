@@ -55,7 +55,11 @@
 namespace dyq {
 
 #ifndef DYQ_PRE_MAX_STAGES
-#define DYQ_PRE_MAX_STAGES 8  // 4 / 6: same block time (316 us): the pipeline depth is not the bound
+// ring depth cap (smem fits 7 stages): round-2 same-box A/B at M = 288, W4A4
+// G64, block: 4 stages 275.0, 5 stages 274.0, 7 stages 280.6 us (gate|up
+// 107.9 / 108.0 / 109.5) -- the depth is not the bound, a shallower ring is
+// slightly faster
+#define DYQ_PRE_MAX_STAGES 5
 #endif
 constexpr int PT = 144;  // tokens per token tile (MMA N)
 static_assert(PT == PRE_PT, "dyq_tp_flag_delta counts prefill token tiles");
