@@ -877,10 +877,24 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
     d2h = out_host.numel() * 2
     n_e2e = min(args.steps, 200)
 
+    side = torch.cuda.Stream()
+
     def e2e_step(k, stream=None):
-        in_dev.copy_(in_host[k], non_blocking=True)
+        # H2D in two parts: [a_{t-1} | x_qkv] ahead of the selector on the step's
+        # stream, the other linears' inputs on a side stream overlapping the
+        # selector and QKV, joined before the o projection
+        cur = stream if stream is not None else torch.cuda.current_stream()
+        hb = in_host[k]
+        in_dev[:offs[1]].copy_(hb[:offs[1]], non_blocking=True)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            in_dev[offs[1]:].copy_(hb[offs[1]:], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(side)
         dyq.select_route(state, 1, a_dev, b_dev, M, row_bits, stream=stream)
         for li in range(len(lins)):
+            if li == 1:
+                cur.wait_event(ev)
             p = packed[k % C][li]
             yo = y_dev if li == len(lins) - 1 else ys[li]
             dyq.qlinear(p.wd, p.codes, p.meta, x_dev[li], M, row_bits, 0, yo, 1, wss[li], stream=stream)
@@ -919,7 +933,8 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": round(dt * 1e3, 4), "steps": n_e2e,
             "path": "public API (select_route + 4 x dyq_qlinear) captured per step index in a CUDA graph with "
-                    "one pinned H2D copy of the step's inputs [a_{t-1} | x x 4] and one D2H copy of [y | b*]; "
+                    "the pinned H2D copy of the step's inputs [a_{t-1} | x x 4] in two parts ([a_{t-1} | x_qkv] "
+                    "first, the rest on a side stream joined before the o projection) and one D2H copy of [y | b*]; "
                     "per step: host writes a_{t-1} into the pinned staging buffer, graph replay, stream sync",
             "eager": {"value": round(bytes_step * world / dt_eager / 1e9, 2),
                       "ms_per_step": round(dt_eager * 1e3, 4),
