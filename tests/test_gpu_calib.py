@@ -22,8 +22,9 @@ DEV = "cuda:0"
 
 
 def _teacher_forced_ok(ref, vis, text, b, a):
-    """Every GPU token of action a (bits b) is the reference argmax, or within
-    bf16-glue noise of it; returns the number of exact decisions."""
+    """Every GPU token of action a (bits b) is the reference argmax, or a
+    near-boundary disagreement within 5e-3 max|logit| of it (the callers allow
+    at most 2 % of those); returns the number of exact decisions."""
     gtok = np.rint((a + 1.0) * 128.0 - 0.5).astype(int)  # detok^-1 (256 bins)
     assert np.array_equal(glue.detok(gtok, 256), a)
     _, logits = ref.episode(vis, text, int(b), forced=gtok)
@@ -63,7 +64,7 @@ def test_policy_step_bits_matches_reference():
         for e in range(E):
             exact += _teacher_forced_ok(ref, vis[e], text[e], bits[e], a[e])
             total += 7
-    assert exact >= 0.9 * total, (exact, total)
+    assert total - exact <= max(1, total // 50), (exact, total)
     with pytest.raises(dyq.DyqError):
         model.step_bits(E, None, t16(vis.reshape(E, -1)), torch.from_numpy(text).to(DEV), act)
 
@@ -106,7 +107,7 @@ def test_calib_collect_end_to_end():
         prev = a[:Ec].copy()
         S_log.append(S.cpu().numpy().copy())
         e_log.append(err.cpu().numpy().copy())
-    assert exact >= 0.9 * total, (exact, total)
+    assert total - exact <= max(1, total // 50), (exact, total)
     Sa, ea = np.concatenate(S_log), np.concatenate(e_log)
     assert np.all(ea >= 0)
     tfp = float(max(Sa.max(), 1e-3))

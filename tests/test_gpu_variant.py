@@ -93,12 +93,12 @@ def _run(model, ref, E, n_vis, n_text, steps, cal_kw, wbits_for, prefill_for=Non
             seen.add(wb)
             _, logits = ref.episode(vis[e], text[e], int(b[e]), forced=gtok, wbits=wb,
                                     prefill=None if prefill_for is None else prefill_for(int(b[e])))
-            top = logits.max(axis=1)
+            top = logits.max(axis=1)  # reference argmax, or a near-boundary flip (<= 2 %)
             tol = 5e-3 * np.abs(logits).max()
             assert np.all(logits[np.arange(7), gtok] >= top - tol), (step, e, gtok, logits.argmax(1))
             exact += int((logits.argmax(axis=1) == gtok).sum())
             total += 7
-    assert exact >= 0.9 * total, (exact, total)
+    assert total - exact <= max(1, total // 50), (exact, total)
     return seen
 
 
