@@ -879,21 +879,26 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
 
     side = torch.cuda.Stream()
 
-    def e2e_step(k, stream=None):
-        # H2D in two parts: [a_{t-1} | x_qkv] ahead of the selector on the step's
-        # stream, the other linears' inputs on a side stream overlapping the
-        # selector and QKV, joined before the o projection
+    def e2e_step(k, stream=None, split=False):
+        # graph form (split): H2D in two parts, [a_{t-1} | x_qkv] ahead of the
+        # selector on the step's stream, the other linears' inputs on a side
+        # stream overlapping the selector and QKV, joined before the o
+        # projection (graph e2e 1203 -> 1233 GB/s same session); eager: one copy
+        # (the host-side fork / join costs more than it hides there)
         cur = stream if stream is not None else torch.cuda.current_stream()
         hb = in_host[k]
-        in_dev[:offs[1]].copy_(hb[:offs[1]], non_blocking=True)
-        side.wait_stream(cur)
-        with torch.cuda.stream(side):
-            in_dev[offs[1]:].copy_(hb[offs[1]:], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(side)
+        if split:
+            in_dev[:offs[1]].copy_(hb[:offs[1]], non_blocking=True)
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                in_dev[offs[1]:].copy_(hb[offs[1]:], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        else:
+            in_dev.copy_(hb, non_blocking=True)
         dyq.select_route(state, 1, a_dev, b_dev, M, row_bits, stream=stream)
         for li in range(len(lins)):
-            if li == 1:
+            if li == 1 and split:
                 cur.wait_event(ev)
             p = packed[k % C][li]
             yo = y_dev if li == len(lins) - 1 else ys[li]
@@ -916,7 +921,7 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
         ge = torch.cuda.CUDAGraph()
         se.wait_stream(torch.cuda.current_stream())
         with torch.cuda.graph(ge, stream=se):
-            e2e_step(k, stream=se)
+            e2e_step(k, stream=se, split=True)
         graphs.append(ge)
     torch.cuda.synchronize()
     ctl.barrier()
