@@ -51,7 +51,7 @@ CASES = [(wb, g, mode) for wb, g in WG for mode in ([2, 4, 8, 16, "mixed"] if (w
 
 
 @pytest.mark.parametrize("name,N,K", synth.LLAMA_BLOCK_LINEARS, ids=[n for n, _, _ in synth.LLAMA_BLOCK_LINEARS])
-@pytest.mark.parametrize("M", [8, 288])
+@pytest.mark.parametrize("M", [1, 3, 8, 288])  # bench m_sweep / policy decode (E = 1) / bench step / prefill
 @pytest.mark.parametrize("WB,G,mode", CASES, ids=[f"W{wb}G{g}-{m}" for wb, g, m in CASES])
 def test_block_linear_fullsize_sampled(name, N, K, M, WB, G, mode):
     seed = zlib.crc32(f"{name}/{M}/{mode}/{WB}/{G}".encode()) % 1000
