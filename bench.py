@@ -872,7 +872,10 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
     y_dev = out_dev[:M * n_last].view(torch.bfloat16).view(M, n_last)
     b_dev = out_dev[M * n_last:].view(torch.int32)
     out_host = torch.empty_like(out_dev, device="cpu").pin_memory()
-    a_host = acts.cpu()
+    a_host = acts.cpu().numpy().reshape(-1, 7)
+    # the host's per-step write of a_{t-1}: numpy views of the pinned staging
+    # buffers (a plain 28-byte store, no tensor-op dispatch)
+    a_stage = [hb.numpy()[:14].view("float32") for hb in in_host]
     h2d = tot * 2
     d2h = out_host.numel() * 2
     n_e2e = min(args.steps, 200)
@@ -911,7 +914,7 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
     tc = time.perf_counter()
     for i in range(n_e2e):
         t = t0 + i
-        in_host[t % 8][:14].view(torch.float32).copy_(a_host[min(t - 1, len(a_host) - 1)].reshape(-1))
+        a_stage[t % 8][:] = a_host[min(t - 1, len(a_host) - 1)]
         e2e_step(t % 8)
         torch.cuda.current_stream().synchronize()
     dt_eager = ctl.reduce((time.perf_counter() - tc) / n_e2e)
@@ -929,7 +932,7 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
     tc = time.perf_counter()
     for i in range(n_e2e):
         t = t0 + i
-        in_host[t % 8][:14].view(torch.float32).copy_(a_host[min(t - 1, len(a_host) - 1)].reshape(-1))
+        a_stage[t % 8][:] = a_host[min(t - 1, len(a_host) - 1)]
         graphs[t % 8].replay()  # enqueued on the current stream
         torch.cuda.current_stream().synchronize()
     dt = ctl.reduce((time.perf_counter() - tc) / n_e2e)
