@@ -909,6 +909,7 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
         out_host.copy_(out_dev, non_blocking=True)
 
     t0 = t_cur + args.steps * (args.trials + 2)
+    cs = torch.cuda.current_stream()  # the step's stream (one object, not one per step)
     ctl.barrier()
     torch.cuda.synchronize()
     tc = time.perf_counter()
@@ -916,7 +917,7 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
         t = t0 + i
         a_stage[t % 8][:] = a_host[min(t - 1, len(a_host) - 1)]
         e2e_step(t % 8)
-        torch.cuda.current_stream().synchronize()
+        cs.synchronize()
     dt_eager = ctl.reduce((time.perf_counter() - tc) / n_e2e)
     se = torch.cuda.Stream()
     graphs = []
@@ -934,7 +935,7 @@ def e2e_leg(args, dyq, torch, dev, lins, packed, xs, ys, wss, state, row_bits, a
         t = t0 + i
         a_stage[t % 8][:] = a_host[min(t - 1, len(a_host) - 1)]
         graphs[t % 8].replay()  # enqueued on the current stream
-        torch.cuda.current_stream().synchronize()
+        cs.synchronize()
     dt = ctl.reduce((time.perf_counter() - tc) / n_e2e)
     del graphs
     return {"value": round(bytes_step * world / dt / 1e9, 2), "unit": "GB/s",
