@@ -715,7 +715,8 @@ static DecPlan dec_plan(const WLayout& L, int nt8) {
     // fit the shared-memory budget.
     static const int stage_code_kb = env_int("DYQ_DEC_STAGE_KB", 56);
     static const int smem_kb1 = env_int("DYQ_DEC_SMEM_KB", 113);
-    const int smem_kb = (nt8 == 1 && DEC_CWARPS == 8) ? smem_kb1 : 200;
+    static const int smem_kb16 = env_int("DYQ_DEC_BUDGET_KB", 200);  // 16-warp build; <= 224 (dynamic-smem attribute)
+    const int smem_kb = (nt8 == 1 && DEC_CWARPS == 8) ? smem_kb1 : (smem_kb16 > 224 ? 224 : smem_kb16);
     const int cps = nt8 * 8 * L.G + nt8 * 64, x16s = nt8 * 8 * L.G * 2;
     for (int want = (stage_code_kb * 1024) / unit_codes;; want /= 2) {
         p.gps = want < 1 ? 1 : (want > L.NG ? L.NG : want);
