@@ -353,6 +353,13 @@ DYQ_API dyq_status_t dyq_attention_prefill(const uint16_t* qkv, int32_t E, int32
 DYQ_API dyq_status_t dyq_attention_decode(const uint16_t* qkv, int32_t E, int32_t pos, int32_t d,
                                           int32_t n_heads, uint16_t* kv, int32_t layer, int32_t n_layers,
                                           int32_t T, uint16_t* out, dyq_stream_t stream);
+/* dyq_rope (rows_per_episode = 1, pos0 = pos) of the q and k parts followed by
+ * dyq_attention_decode, in one kernel: the rotated k goes into the cache, qkv
+ * is left unrotated; bit-identical to the two calls.  qkv and kv 16-B aligned
+ * and d % 8 == 0, else DYQ_EUNSUPPORTED (nothing launched). */
+DYQ_API dyq_status_t dyq_attention_decode_rope(const uint16_t* qkv, int32_t E, int32_t pos, int32_t d,
+                                               int32_t n_heads, float theta, uint16_t* kv, int32_t layer,
+                                               int32_t n_layers, int32_t T, uint16_t* out, dyq_stream_t stream);
 /* act[m, j] = SiLU(gu[m, j]) * gu[m, ffn + j] */
 DYQ_API dyq_status_t dyq_silu_mul(const uint16_t* gu, int32_t M, int32_t ffn, uint16_t* act,
                                   dyq_stream_t stream);

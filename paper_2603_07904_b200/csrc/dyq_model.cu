@@ -120,6 +120,19 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// rotate_half RoPE of one pair (i, i + HD/2) at position pos: the one
+// definition rope_kernel and the fused decode attention (attn_decode2_kernel
+// with theta > 0) share, with explicit roundings (no contraction), so the two
+// paths give the same bits
+__device__ __forceinline__ void rope_pair(float x1, float x2, float pos, int i, float theta, uint16_t& o1,
+                                          uint16_t& o2) {
+    const float inv_freq = powf(theta, -2.f * (float)i / (float)HD);
+    float sn, cs;
+    sincosf(__fmul_rn(pos, inv_freq), &sn, &cs);
+    o1 = f2bf(__fsub_rn(__fmul_rn(x1, cs), __fmul_rn(x2, sn)));
+    o2 = f2bf(__fadd_rn(__fmul_rn(x2, cs), __fmul_rn(x1, sn)));
+}
+
 // rotate_half RoPE on the q and k parts: pairs (i, i + HD/2) of every head
 __global__ void rope_kernel(uint16_t* __restrict__ qkv, int M, int S, int pos0, int d, int H, float theta) {
     ptx::pdl_wait();
@@ -132,14 +145,8 @@ __global__ void rope_kernel(uint16_t* __restrict__ qkv, int M, int S, int pos0, 
     const int r = (int)(idx % per_row);
     const int which = r / (H * half);  // 0 = q, 1 = k
     const int hh = (r / half) % H, i = r % half;
-    const float pos = (float)(m % S + pos0);
-    const float inv_freq = powf(theta, -2.f * (float)i / (float)HD);
-    float sn, cs;
-    sincosf(pos * inv_freq, &sn, &cs);
     uint16_t* p = qkv + (size_t)m * 3 * d + (size_t)which * d + hh * HD;
-    const float x1 = bf2f(p[i]), x2 = bf2f(p[i + half]);
-    p[i] = f2bf(x1 * cs - x2 * sn);
-    p[i + half] = f2bf(x2 * cs + x1 * sn);
+    rope_pair(bf2f(p[i]), bf2f(p[i + half]), (float)(m % S + pos0), i, theta, p[i], p[i + half]);
 }
 
 __device__ __forceinline__ size_t kv_off(int e, int l, int kv, int pos, int L, int T, int d) {
@@ -487,9 +494,11 @@ __global__ void __launch_bounds__(256) attn_decode_kernel(const uint16_t* __rest
 // key slice of 32), 16-B value loads, partial sums reduced through shared
 // memory.  PDL-launched.
 constexpr int ADT = 512;
+// theta > 0: RoPE of this head's q and new k applied here (rope_pair, the
+// rope_kernel arithmetic) instead of by a separate rope_kernel launch.
 __global__ void __launch_bounds__(ADT) attn_decode2_kernel(const uint16_t* __restrict__ qkv, int pos, int d, int H,
                                                            uint16_t* __restrict__ kv, int layer, int L, int T,
-                                                           uint16_t* __restrict__ out) {
+                                                           uint16_t* __restrict__ out, float theta) {
     extern __shared__ __align__(16) float smf[];
     float* qsh = smf;            // [HD]
     float* red = qsh + HD;       // [32]
@@ -504,13 +513,32 @@ __global__ void __launch_bounds__(ADT) attn_decode2_kernel(const uint16_t* __res
     uint16_t* Vc = kv + kv_off(e, layer, 1, 0, L, T, d) + hh * HD;
     const float scale = rsqrtf((float)HD);
     const int tid = threadIdx.x;
-    if (tid < HD / 8) {
-        *reinterpret_cast<uint4*>(Kc + (size_t)pos * d + tid * 8) =
-            *reinterpret_cast<const uint4*>(row + d + hh * HD + tid * 8);
-        *reinterpret_cast<uint4*>(Vc + (size_t)pos * d + tid * 8) =
-            *reinterpret_cast<const uint4*>(row + 2 * d + hh * HD + tid * 8);
+    if (theta > 0.f) {
+        if (tid < HD / 8)
+            *reinterpret_cast<uint4*>(Vc + (size_t)pos * d + tid * 8) =
+                *reinterpret_cast<const uint4*>(row + 2 * d + hh * HD + tid * 8);
+        if (tid < HD) {  // threads [0, HD/2): q pairs, [HD/2, HD): k pairs
+            const int i = tid & (HD / 2 - 1);
+            const uint16_t* src = row + (tid < HD / 2 ? 0 : d) + hh * HD;
+            uint16_t o1, o2;
+            rope_pair(bf2f(src[i]), bf2f(src[i + HD / 2]), (float)pos, i, theta, o1, o2);
+            if (tid < HD / 2) {
+                qsh[i] = bf2f(o1) * scale;
+                qsh[i + HD / 2] = bf2f(o2) * scale;
+            } else {
+                Kc[(size_t)pos * d + i] = o1;
+                Kc[(size_t)pos * d + i + HD / 2] = o2;
+            }
+        }
+    } else {
+        if (tid < HD / 8) {
+            *reinterpret_cast<uint4*>(Kc + (size_t)pos * d + tid * 8) =
+                *reinterpret_cast<const uint4*>(row + d + hh * HD + tid * 8);
+            *reinterpret_cast<uint4*>(Vc + (size_t)pos * d + tid * 8) =
+                *reinterpret_cast<const uint4*>(row + 2 * d + hh * HD + tid * 8);
+        }
+        if (tid < HD) qsh[tid] = bf2f(row[hh * HD + tid]) * scale;
     }
-    if (tid < HD) qsh[tid] = bf2f(row[hh * HD + tid]) * scale;
     __syncthreads();
     float mx = -INFINITY;
     for (int j = tid; j <= pos; j += ADT) {
@@ -966,8 +994,16 @@ dyq_status_t dyq_attention_prefill(const uint16_t* qkv, int32_t E, int32_t S, in
     return check_launch("attn_prefill_kernel");
 }
 
-dyq_status_t dyq_attention_decode(const uint16_t* qkv, int32_t E, int32_t pos, int32_t d, int32_t H, uint16_t* kv,
-                                  int32_t layer, int32_t L, int32_t T, uint16_t* out, dyq_stream_t stream) {
+}  // extern "C"
+
+namespace dyq {
+// Decode attention; theta > 0 also applies RoPE to the step's q and new k
+// (the policy step's fused path).  The fused form needs the aligned kernel:
+// on a misaligned buffer the caller falls back to dyq_rope + the generic
+// kernel (returns DYQ_EUNSUPPORTED without launching).
+static dyq_status_t attention_decode(const uint16_t* qkv, int32_t E, int32_t pos, int32_t d, int32_t H, uint16_t* kv,
+                                     int32_t layer, int32_t L, int32_t T, uint16_t* out, float theta,
+                                     cudaStream_t stream) {
     if (E <= 0 || pos < 0 || pos >= T || d != H * HD || layer < 0 || layer >= L)
         return set_error(DYQ_ESHAPE, "bad attention shape");
     if (d % 8 == 0 && ((uintptr_t)qkv | (uintptr_t)kv) % 16 == 0) {
@@ -979,14 +1015,31 @@ dyq_status_t dyq_attention_decode(const uint16_t* qkv, int32_t E, int32_t pos, i
                 attr = true;
             }
         }
-        const cudaError_t e = launch_pdl(attn_decode2_kernel, dim3(H, E), dim3(ADT), smem2, (cudaStream_t)stream, qkv,
-                                         pos, d, H, kv, layer, L, T, out);
+        const cudaError_t e = launch_pdl(attn_decode2_kernel, dim3(H, E), dim3(ADT), smem2, stream, qkv, pos, d, H, kv,
+                                         layer, L, T, out, theta);
         if (e != cudaSuccess) return set_error(DYQ_ECUDA, "attn_decode2_kernel: %s", cudaGetErrorString(e));
         return check_launch("attn_decode2_kernel");
     }
+    if (theta > 0.f) return DYQ_EUNSUPPORTED;
     const size_t smem = (HD + (size_t)(pos + 1) + 32 + 4 * HD) * 4;
-    attn_decode_kernel<<<dim3(H, E), 256, smem, (cudaStream_t)stream>>>(qkv, pos, d, H, kv, layer, L, T, out);
+    attn_decode_kernel<<<dim3(H, E), 256, smem, stream>>>(qkv, pos, d, H, kv, layer, L, T, out);
     return check_launch("attn_decode_kernel");
+}
+}  // namespace dyq
+
+extern "C" {
+dyq_status_t dyq_attention_decode(const uint16_t* qkv, int32_t E, int32_t pos, int32_t d, int32_t H, uint16_t* kv,
+                                  int32_t layer, int32_t L, int32_t T, uint16_t* out, dyq_stream_t stream) {
+    return attention_decode(qkv, E, pos, d, H, kv, layer, L, T, out, 0.f, (cudaStream_t)stream);
+}
+
+dyq_status_t dyq_attention_decode_rope(const uint16_t* qkv, int32_t E, int32_t pos, int32_t d, int32_t H, float theta,
+                                       uint16_t* kv, int32_t layer, int32_t L, int32_t T, uint16_t* out,
+                                       dyq_stream_t stream) {
+    if (!(theta > 0.f)) return set_error(DYQ_EINVAL, "rope theta must be positive");
+    const dyq_status_t rc = attention_decode(qkv, E, pos, d, H, kv, layer, L, T, out, theta, (cudaStream_t)stream);
+    if (rc == DYQ_EUNSUPPORTED) return set_error(DYQ_EUNSUPPORTED, "fused rope + attention needs 16-B aligned qkv / kv");
+    return rc;
 }
 
 dyq_status_t dyq_silu_mul(const uint16_t* gu, int32_t M, int32_t ffn, uint16_t* act, dyq_stream_t stream) {
@@ -1210,11 +1263,20 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
         -> dyq_status_t {
         const size_t li = (size_t)4 * l;
         DYQ_TRY(qlin(0, li, xn, M, rb, rb8, g, qkv, false));
-        DYQ_TRY(dyq_rope(qkv, M, prefill ? S : 1, prefill ? 0 : pos, d, H, D.rope_theta, stream));
-        if (prefill)
+        if (prefill) {
+            DYQ_TRY(dyq_rope(qkv, M, S, 0, d, H, D.rope_theta, stream));
             DYQ_TRY(dyq_attention_prefill(qkv, E, S, d, H, kv, l, NL, L.T, att, stream));
-        else
-            DYQ_TRY(dyq_attention_decode(qkv, E, pos, d, H, kv, l, NL, L.T, att, stream));
+        } else {
+            // RoPE inside the decode attention kernel (one launch less per layer
+            // and decode pass); the separate kernels where the fused one cannot run
+            rc = attention_decode(qkv, E, pos, d, H, kv, l, NL, L.T, att, D.rope_theta, st);
+            if (rc == DYQ_EUNSUPPORTED) {
+                DYQ_TRY(dyq_rope(qkv, M, 1, pos, d, H, D.rope_theta, stream));
+                DYQ_TRY(dyq_attention_decode(qkv, E, pos, d, H, kv, l, NL, L.T, att, stream));
+            } else if (rc) {
+                return rc;
+            }
+        }
         DYQ_TRY(qlin(1, li, att, M, rb, rb8, g, delta, false));
         DYQ_TRY(dyq_add_rmsnorm(h, delta, D.mlp_norm + (size_t)l * d, M, d, D.rms_eps, xn, stream));
         DYQ_TRY(qlin(2, li, xn, M, rb, rb8, g, gu, false));

@@ -54,6 +54,7 @@ _SIGS = {
     "dyq_rope": [P, i32, i32, i32, i32, i32, C.c_float, P],
     "dyq_attention_prefill": [P, i32, i32, i32, i32, P, i32, i32, i32, P, P],
     "dyq_attention_decode": [P, i32, i32, i32, i32, P, i32, i32, i32, P, P],
+    "dyq_attention_decode_rope": [P, i32, i32, i32, i32, C.c_float, P, i32, i32, i32, P, P],
     "dyq_silu_mul": [P, i32, i32, P, P],
     "dyq_head_argmax": [P, i32, i32, i32, P, i32, P, P, i32, P],
     "dyq_tp_shard": [i32, i32, i32, P, P],
@@ -385,6 +386,12 @@ def attention_decode(qkv, E: int, pos: int, d: int, n_heads: int, kv, layer: int
                      stream=None):
     _call("dyq_attention_decode", _ptr(qkv), E, pos, d, n_heads, _ptr(kv), layer, n_layers, T, _ptr(out),
           _stream(stream))
+
+
+def attention_decode_rope(qkv, E: int, pos: int, d: int, n_heads: int, theta: float, kv, layer: int, n_layers: int,
+                          T: int, out, stream=None):
+    _call("dyq_attention_decode_rope", _ptr(qkv), E, pos, d, n_heads, theta, _ptr(kv), layer, n_layers, T,
+          _ptr(out), _stream(stream))
 
 
 def silu_mul(gu, M: int, ffn: int, act, stream=None):

@@ -103,6 +103,29 @@ def test_attention_decode(E, pos):
         assert np.array_equal(kvg[e, 1, 0, pos], glue.to_bf16_bits(x[e, d:2 * d]))
 
 
+@pytest.mark.parametrize("E,pos", [(1, 0), (1, 7), (3, 200), (8, 294)])
+def test_attention_decode_rope_fused_equals_two_kernels(E, pos):
+    """The policy step's fused RoPE + decode attention vs dyq_rope followed by
+    dyq_attention_decode: same output and same cache bits; qkv left unrotated."""
+    d, H, L, T = 512, 4, 2, 295
+    rng = np.random.default_rng(60 + pos)
+    kvh = glue.to_bf16_bits(rng.standard_normal((E, L, 2, T, d)))
+    qkv0 = rnd_bits((E, 3 * d), 61 + E)
+    kv_a, kv_b = t16(kvh.reshape(-1)), t16(kvh.reshape(-1))
+    out_a = torch.empty(E, d, dtype=torch.int16, device=DEV)
+    out_b = torch.empty(E, d, dtype=torch.int16, device=DEV)
+    qa, qb = t16(qkv0), t16(qkv0)
+    dyq.attention_decode_rope(qa, E, pos, d, H, 10000.0, kv_a, 1, L, T, out_a)
+    dyq.rope(qb, E, 1, pos, d, H, 10000.0)
+    dyq.attention_decode(qb, E, pos, d, H, kv_b, 1, L, T, out_b)
+    torch.cuda.synchronize()
+    assert torch.equal(out_a, out_b)
+    assert torch.equal(kv_a, kv_b)
+    assert np.array_equal(qa.cpu().numpy().view(np.uint16), qkv0)  # fused path leaves qkv unrotated
+    with pytest.raises(dyq.DyqError):
+        dyq.attention_decode_rope(_misaligned(qkv0), E, pos, d, H, 10000.0, kv_a, 1, L, T, out_a)
+
+
 def test_silu_mul_and_head():
     M, ffn = 9, 1024
     gu0 = rnd_bits((M, 2 * ffn), 8, 3.0)
