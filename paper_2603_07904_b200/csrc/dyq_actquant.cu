@@ -24,79 +24,10 @@ __global__ void actquant_dec_kernel(WLayout L, const uint16_t* __restrict__ x, i
     ptx::pdl_wait();  // x may be produced by the preceding kernel
     if (threadIdx.x == 0) trace_ev(trace, serial, 2, 1);
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
     const int MP = 8 * A.nt8;
     if (warp >= MP * L.NG) return;
     const int g = warp / MP, m = warp % MP;
-    uint8_t* rec = ws + A.cp_off + (size_t)g * A.cp_stride;
-    uint8_t* dq = rec + (size_t)m * L.G;
-    uint16_t* d16 = reinterpret_cast<uint16_t*>(ws + A.x16_off + (size_t)g * A.x16_stride) + (size_t)m * L.G;
-    uint2* pdst = reinterpret_cast<uint2*>(rec + MP * L.G) + m;
-    uint8_t* zdst = ws + A.zx_off + (size_t)g * DEC_MPAD + m;
-    const int b = (m < M) ? (row_bits ? row_bits[m0 + m] : bits) : 0;
-    const bool centred = dec_call_centred(M, m0, row_bits, bits);
-    // gated: x = [g | u] rows of width 2K (SwiGLU input); the activation is
-    // bf16(silu(g) * u), the same float ops as silu_mul_kernel (dyq_model.cu)
-    const uint16_t* src = x + (size_t)(m0 + m) * L.K * (gated ? 2 : 1) + (size_t)g * L.G;
-    constexpr int MAXV = 4;  // G <= 128
-    float v[MAXV];
-    uint16_t raw[MAXV];
-    float vmin = 0.f, vmax = 0.f;
-    int bad = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
-        const int k = lane + 32 * i;
-        v[i] = 0.f;
-        raw[i] = 0;
-        if (k < L.G && b != 0) {
-            raw[i] = gated ? silu_mul_bf16(src[k], src[k + L.K]) : src[k];
-            v[i] = bf16_bits_to_float(raw[i]);
-            if (!finite_f(v[i])) bad = min(bad, k);
-            vmin = fminf(vmin, v[i]);
-            vmax = fmaxf(vmax, v[i]);
-        }
-    }
-    bad = warp_min_i(bad);
-    if (bad != 0x7fffffff && lane == 0)
-        report_nonfinite(err, (int64_t)(m0 + m) * L.K + (int64_t)g * L.G + bad);
-    if (b != 2 && b != 4 && b != 8) {  // padding row or BF16 bypass row
-#pragma unroll
-        for (int i = 0; i < MAXV; ++i) {
-            const int k = lane + 32 * i;
-            if (k < L.G) {
-                const int pos = (k & ~63) + dec_perm(k & 63);
-                dq[pos] = 0;
-                d16[pos] = (b == 16) ? raw[i] : (uint16_t)0;
-            }
-        }
-        if (lane == 0) {
-            *pdst = make_uint2(0u, 0u);
-            *zdst = 0;
-        }
-        return;
-    }
-    vmin = warp_min(vmin);
-    vmax = warp_max(vmax);
-    float s;
-    int z;
-    fit_params(vmin, vmax, b, &s, &z);
-    int sum = 0;
-#pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
-        const int k = lane + 32 * i;
-        if (k < L.G) {
-            const int q = quantize_one(v[i], s, z, b, L.round_mode);
-            sum += q;
-            const int pos = (k & ~63) + dec_perm(k & 63);
-            dq[pos] = centred ? (uint8_t)(int8_t)(q - z) : (uint8_t)q;
-            d16[pos] = 0;
-        }
-    }
-    sum = warp_sum_i(sum);
-    if (lane == 0) {
-        *pdst = make_uint2(__float_as_uint(s), centred ? (uint32_t)(sum - L.G * z) : ((uint32_t)z << 16) | (uint32_t)sum);
-        *zdst = (uint8_t)z;
-    }
+    aq_dec_job(L, x, M, m0, row_bits, bits, ws, A, err, gated, g, m, dec_call_centred(M, m0, row_bits, bits));
     if (threadIdx.x == 0) trace_ev(trace, serial, 2, 2);
 }
 

@@ -264,6 +264,11 @@ dyq_status_t dyq_route_bits(const int32_t* bits, int32_t E, int32_t tpe, const i
 // Workspace = [decode split-K accumulator + tile counters (must start zeroed;
 // self-cleaning)] [standalone activation-quantizer output (dyq_act_quant)].
 static size_t act_area_offset(const WLayout& L) { return (decode_ws_bytes(L) + 255) & ~(size_t)255; }
+}  // extern "C"
+namespace dyq {
+uint8_t* dec_act_area(const WLayout& L, void* ws) { return reinterpret_cast<uint8_t*>(ws) + act_area_offset(L); }
+}  // namespace dyq
+extern "C" {
 // The 1 KB before the prefill area holds the prefill stream-K unit counters
 // (fixed position per shape, so they stay zeroed for every M; self-resetting).
 static size_t prefill_area_offset(const WLayout& L) {

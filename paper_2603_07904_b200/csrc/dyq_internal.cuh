@@ -224,7 +224,90 @@ __device__ inline float warp_max(float v) { return ord2f(__reduce_max_sync(0xfff
 __device__ inline int warp_sum_i(int v) { return __reduce_add_sync(0xffffffffu, v); }
 __device__ inline int warp_min_i(int v) { return __reduce_min_sync(0xffffffffu, v); }
 
+// One decode-quantizer job (a whole warp): token row m (of rows m0 ..) and
+// K-group g of x at the row's bits into the decode activation layout (records
+// codes at dec_perm positions + {s_x, z_x << 16 | SX} or, centred, {s_x,
+// SXc}; bf16 copies of BF16-bypass rows in x16; z_x bytes).  m >= M: padding
+// row (zeros).  Used by actquant_dec_kernel and by the decode attention
+// kernel's epilogue (the o projection's input, dyq_model.cu).
+__device__ inline void aq_dec_job(const WLayout& L, const uint16_t* __restrict__ x, int M, int m0,
+                                  const int32_t* __restrict__ row_bits, int bits, uint8_t* __restrict__ ws,
+                                  const ActLayoutDec& A, int64_t* err, int gated, int g, int m, bool centred) {
+    const int lane = threadIdx.x & 31;
+    const int MP = 8 * A.nt8;
+    uint8_t* rec = ws + A.cp_off + (size_t)g * A.cp_stride;
+    uint8_t* dq = rec + (size_t)m * L.G;
+    uint16_t* d16 = reinterpret_cast<uint16_t*>(ws + A.x16_off + (size_t)g * A.x16_stride) + (size_t)m * L.G;
+    uint2* pdst = reinterpret_cast<uint2*>(rec + MP * L.G) + m;
+    uint8_t* zdst = ws + A.zx_off + (size_t)g * DEC_MPAD + m;
+    const int b = (m < M) ? (row_bits ? row_bits[m0 + m] : bits) : 0;
+    // gated: x = [g | u] rows of width 2K (SwiGLU input); the activation is
+    // bf16(silu(g) * u), the same float ops as silu_mul_kernel (dyq_model.cu)
+    const uint16_t* src = x + (size_t)(m0 + m) * L.K * (gated ? 2 : 1) + (size_t)g * L.G;
+    constexpr int MAXV = 4;  // G <= 128
+    float v[MAXV];
+    uint16_t raw[MAXV];
+    float vmin = 0.f, vmax = 0.f;
+    int bad = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+        const int k = lane + 32 * i;
+        v[i] = 0.f;
+        raw[i] = 0;
+        if (k < L.G && b != 0) {
+            raw[i] = gated ? silu_mul_bf16(src[k], src[k + L.K]) : src[k];
+            v[i] = bf16_bits_to_float(raw[i]);
+            if (!finite_f(v[i])) bad = min(bad, k);
+            vmin = fminf(vmin, v[i]);
+            vmax = fmaxf(vmax, v[i]);
+        }
+    }
+    bad = warp_min_i(bad);
+    if (bad != 0x7fffffff && lane == 0)
+        report_nonfinite(err, (int64_t)(m0 + m) * L.K + (int64_t)g * L.G + bad);
+    if (b != 2 && b != 4 && b != 8) {  // padding row or BF16 bypass row
+#pragma unroll
+        for (int i = 0; i < MAXV; ++i) {
+            const int k = lane + 32 * i;
+            if (k < L.G) {
+                const int pos = (k & ~63) + dec_perm(k & 63);
+                dq[pos] = 0;
+                d16[pos] = (b == 16) ? raw[i] : (uint16_t)0;
+            }
+        }
+        if (lane == 0) {
+            *pdst = make_uint2(0u, 0u);
+            *zdst = 0;
+        }
+        return;
+    }
+    vmin = warp_min(vmin);
+    vmax = warp_max(vmax);
+    float s;
+    int z;
+    fit_params(vmin, vmax, b, &s, &z);
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+        const int k = lane + 32 * i;
+        if (k < L.G) {
+            const int q = quantize_one(v[i], s, z, b, L.round_mode);
+            sum += q;
+            const int pos = (k & ~63) + dec_perm(k & 63);
+            dq[pos] = centred ? (uint8_t)(int8_t)(q - z) : (uint8_t)q;
+            d16[pos] = 0;
+        }
+    }
+    sum = warp_sum_i(sum);
+    if (lane == 0) {
+        *pdst = make_uint2(__float_as_uint(s), centred ? (uint32_t)(sum - L.G * z) : ((uint32_t)z << 16) | (uint32_t)sum);
+        *zdst = (uint8_t)z;
+    }
+}
+
 size_t decode_ws_bytes(const WLayout& L);
+// the decode activation area (actquant_dec_kernel's output) of a qlinear workspace
+uint8_t* dec_act_area(const WLayout& L, void* ws);
 dyq_status_t launch_prefetch_l2(const void* p, size_t bytes, cudaStream_t st);
 PreActLayout pre_act_layout(const WLayout& L, int M);
 // prefill stream-K: the largest number of CTAs sharing one output tile (1 =

@@ -494,11 +494,26 @@ __global__ void __launch_bounds__(256) attn_decode_kernel(const uint16_t* __rest
 // key slice of 32), 16-B value loads, partial sums reduced through shared
 // memory.  PDL-launched.
 constexpr int ADT = 512;
+// Quantization of the attention output for the o projection inside the
+// attention kernel (policy step): ws = the o linear's decode activation area
+// (null: off), rows 0 .. M-1 = episodes.
+struct OQuant {
+    uint8_t* ws;
+    ActLayoutDec A;
+    WLayout L;
+    const int32_t* row_bits;
+    int bits, M;
+    int64_t* err;
+};
+
 // theta > 0: RoPE of this head's q and new k applied here (rope_pair, the
 // rope_kernel arithmetic) instead of by a separate rope_kernel launch.
+// oq.ws != null: the CTA then quantizes its head's output groups (and, for
+// episode 0, the padding rows of those groups) with aq_dec_job -- the o
+// projection's act-quant kernel is not launched.
 __global__ void __launch_bounds__(ADT) attn_decode2_kernel(const uint16_t* __restrict__ qkv, int pos, int d, int H,
                                                            uint16_t* __restrict__ kv, int layer, int L, int T,
-                                                           uint16_t* __restrict__ out, float theta) {
+                                                           uint16_t* __restrict__ out, float theta, OQuant oq) {
     extern __shared__ __align__(16) float smf[];
     float* qsh = smf;            // [HD]
     float* red = qsh + HD;       // [32]
@@ -612,6 +627,17 @@ __global__ void __launch_bounds__(ADT) attn_decode2_kernel(const uint16_t* __res
 #pragma unroll 8
         for (int q = 0; q < 32; ++q) acc += part[q * HD + tid];
         out[(size_t)e * d + hh * HD + tid] = f2bf(acc / sum);
+    }
+    if (oq.ws) {
+        __syncthreads();  // this CTA's HD outputs of row e are written (CTA-visible)
+        const int G = oq.L.G, gph = HD / G, MP = 8 * oq.A.nt8;
+        const bool centred = dec_call_centred(oq.M, 0, oq.row_bits, oq.bits);
+        const int jobs = gph * (1 + (e == 0 ? MP - oq.M : 0));
+        for (int jb = tid >> 5; jb < jobs; jb += ADT / 32) {
+            const int gi = jb % gph, r = jb / gph;
+            aq_dec_job(oq.L, out, oq.M, 0, oq.row_bits, oq.bits, oq.ws, oq.A, oq.err, 0, hh * gph + gi,
+                       r == 0 ? e : oq.M + r - 1, centred);
+        }
     }
 }
 
@@ -1003,7 +1029,7 @@ namespace dyq {
 // kernel (returns DYQ_EUNSUPPORTED without launching).
 static dyq_status_t attention_decode(const uint16_t* qkv, int32_t E, int32_t pos, int32_t d, int32_t H, uint16_t* kv,
                                      int32_t layer, int32_t L, int32_t T, uint16_t* out, float theta,
-                                     cudaStream_t stream) {
+                                     cudaStream_t stream, const OQuant& oq = OQuant{}) {
     if (E <= 0 || pos < 0 || pos >= T || d != H * HD || layer < 0 || layer >= L)
         return set_error(DYQ_ESHAPE, "bad attention shape");
     if (d % 8 == 0 && ((uintptr_t)qkv | (uintptr_t)kv) % 16 == 0) {
@@ -1016,11 +1042,11 @@ static dyq_status_t attention_decode(const uint16_t* qkv, int32_t E, int32_t pos
             }
         }
         const cudaError_t e = launch_pdl(attn_decode2_kernel, dim3(H, E), dim3(ADT), smem2, stream, qkv, pos, d, H, kv,
-                                         layer, L, T, out, theta);
+                                         layer, L, T, out, theta, oq);
         if (e != cudaSuccess) return set_error(DYQ_ECUDA, "attn_decode2_kernel: %s", cudaGetErrorString(e));
         return check_launch("attn_decode2_kernel");
     }
-    if (theta > 0.f) return DYQ_EUNSUPPORTED;
+    if (theta > 0.f || oq.ws) return DYQ_EUNSUPPORTED;
     const size_t smem = (HD + (size_t)(pos + 1) + 32 + 4 * HD) * 4;
     attn_decode_kernel<<<dim3(H, E), 256, smem, stream>>>(qkv, pos, d, H, kv, layer, L, T, out);
     return check_launch("attn_decode_kernel");
@@ -1186,6 +1212,8 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
     int32_t* rb8d = m->at<int32_t>(L.rb8d);
     int32_t* gates = m->at<int32_t>(L.gates);  // [W4 prefill, W8 prefill, W4 decode, W8 decode]
     const bool w8 = L.w8 && !forced;           // forced-bits steps (calibration) stay on the W4 table
+    const char* fo = getenv("DYQ_FUSE_OQ");     // 0: the o projection's separate act-quant kernel (A/B, tests)
+    const bool fuse_oq = !(fo && atoi(fo) == 0);
     const bool paper = D.paper_mode && !forced && m->side;
     const int pre_bits = D.prefill_bits ? D.prefill_bits : 16;
     int4 wtab = make_int4(4, 4, 4, 4), atab = make_int4(2, 4, 8, 16);
@@ -1263,21 +1291,42 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
         -> dyq_status_t {
         const size_t li = (size_t)4 * l;
         DYQ_TRY(qlin(0, li, xn, M, rb, rb8, g, qkv, false));
+        bool o_done = false;
         if (prefill) {
             DYQ_TRY(dyq_rope(qkv, M, S, 0, d, H, D.rope_theta, stream));
             DYQ_TRY(dyq_attention_prefill(qkv, E, S, d, H, kv, l, NL, L.T, att, stream));
         } else {
             // RoPE inside the decode attention kernel (one launch less per layer
-            // and decode pass); the separate kernels where the fused one cannot run
-            rc = attention_decode(qkv, E, pos, d, H, kv, l, NL, L.T, att, D.rope_theta, st);
+            // and decode pass), and -- W4-pinned table, M <= 16 -- the o
+            // projection's activation quantization in its epilogue (one more);
+            // the separate kernels where the fused ones cannot run
+            OQuant oq{};
+            WLayout Lo;
+            const bool fuse_o = fuse_oq && !(w8 && rb8 != nullptr) && M <= DEC_MPAD && make_layout(&wd[1], &Lo);
+            if (fuse_o) {
+                oq.ws = dec_act_area(Lo, ws[1]);
+                oq.A = act_layout_dec(Lo, dec_nt8(M));
+                oq.L = Lo;
+                oq.row_bits = rb;
+                oq.bits = 0;
+                oq.M = M;
+                oq.err = err;
+            }
+            rc = attention_decode(qkv, E, pos, d, H, kv, l, NL, L.T, att, D.rope_theta, st, oq);
             if (rc == DYQ_EUNSUPPORTED) {
                 DYQ_TRY(dyq_rope(qkv, M, 1, pos, d, H, D.rope_theta, stream));
                 DYQ_TRY(dyq_attention_decode(qkv, E, pos, d, H, kv, l, NL, L.T, att, stream));
             } else if (rc) {
                 return rc;
+            } else {
+                o_done = fuse_o;
             }
         }
-        DYQ_TRY(qlin(1, li, att, M, rb, rb8, g, delta, false));
+        if (o_done)  // o projection on the records the attention kernel wrote
+            DYQ_TRY(dyq_qlinear_q(&wd[1], m->codes[li + 1], m->meta[li + 1], att, M, rb, 0, delta, 1, ws[1],
+                                  L.ws_bytes[1], stream));
+        else
+            DYQ_TRY(qlin(1, li, att, M, rb, rb8, g, delta, false));
         DYQ_TRY(dyq_add_rmsnorm(h, delta, D.mlp_norm + (size_t)l * d, M, d, D.rms_eps, xn, stream));
         DYQ_TRY(qlin(2, li, xn, M, rb, rb8, g, gu, false));
         // SwiGLU fused into the down projection's activation quantization

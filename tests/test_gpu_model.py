@@ -214,6 +214,37 @@ def test_policy_step_matches_reference_and_selector():
     assert total - exact <= max(1, total // 50), (exact, total)
 
 
+@pytest.mark.parametrize("E", [1, 3])
+def test_policy_step_fused_o_quant_is_bit_identical(E, monkeypatch):
+    """The decode passes quantize the o projection's input in the attention
+    kernel's epilogue (aq_dec_job, the standalone quantizer's own code); with
+    DYQ_FUSE_OQ=0 the separate act-quant kernel runs.  Same actions, bits and
+    KV cache either way."""
+    n_vis, n_text = 8, 4
+    w = _tiny(5)
+    cal = dyq.default_calib()
+    res = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("DYQ_FUSE_OQ", fuse)
+        model = _gpu_model(w, E, n_vis, n_text)
+        state = torch.zeros(dyq.state_size(E, cal), dtype=torch.uint8, device=DEV)
+        dyq.state_init(E, cal, state)
+        rng = np.random.default_rng(77)
+        act = torch.zeros(E, 7, dtype=torch.float32, device=DEV)
+        bits = torch.zeros(E, dtype=torch.int32, device=DEV)
+        out = []
+        for _ in range(12):
+            vis = glue.to_bf16_bits(rng.standard_normal((E, n_vis, 256)))
+            text = rng.integers(0, 256, (E, n_text)).astype(np.int32)
+            model.step(state, E, t16(vis.reshape(E, -1)), torch.from_numpy(text).to(DEV), act, bits)
+            out.append((act.cpu().numpy().copy(), bits.cpu().numpy().copy()))
+        torch.cuda.synchronize()
+        res.append((out, model.kv.cpu().numpy().copy()))
+    for (a1, b1), (a2, b2) in zip(res[0][0], res[1][0]):
+        assert np.array_equal(a1.view(np.uint32), a2.view(np.uint32)) and np.array_equal(b1, b2)
+    assert np.array_equal(res[0][1], res[1][1])
+
+
 def test_policy_step_repeat_is_deterministic():
     E, n_vis, n_text = 3, 8, 4
     w = _tiny(1)
