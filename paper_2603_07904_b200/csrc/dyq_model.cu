@@ -508,9 +508,8 @@ struct OQuant {
 
 // theta > 0: RoPE of this head's q and new k applied here (rope_pair, the
 // rope_kernel arithmetic) instead of by a separate rope_kernel launch.
-// oq.ws != null: the CTA then quantizes its head's output groups (and, for
-// episode 0, the padding rows of those groups) with aq_dec_job -- the o
-// projection's act-quant kernel is not launched.
+// oq.ws != null: the CTA then quantizes its head's output groups with
+// aq_dec_job -- the o projection's act-quant kernel is not launched.
 __global__ void __launch_bounds__(ADT) attn_decode2_kernel(const uint16_t* __restrict__ qkv, int pos, int d, int H,
                                                            uint16_t* __restrict__ kv, int layer, int L, int T,
                                                            uint16_t* __restrict__ out, float theta, OQuant oq) {
@@ -630,15 +629,78 @@ __global__ void __launch_bounds__(ADT) attn_decode2_kernel(const uint16_t* __res
     }
     if (oq.ws) {
         __syncthreads();  // this CTA's HD outputs of row e are written (CTA-visible)
-        const int G = oq.L.G, gph = HD / G, MP = 8 * oq.A.nt8;
+        // (padding rows M .. 8 nt8 - 1 of the records are left as they are: the
+        // decode kernel's token columns are independent, padding columns never stored)
+        const int gph = HD / oq.L.G;
         const bool centred = dec_call_centred(oq.M, 0, oq.row_bits, oq.bits);
-        const int jobs = gph * (1 + (e == 0 ? MP - oq.M : 0));
-        for (int jb = tid >> 5; jb < jobs; jb += ADT / 32) {
-            const int gi = jb % gph, r = jb / gph;
-            aq_dec_job(oq.L, out, oq.M, 0, oq.row_bits, oq.bits, oq.ws, oq.A, oq.err, 0, hh * gph + gi,
-                       r == 0 ? e : oq.M + r - 1, centred);
+        for (int gi = tid >> 5; gi < gph; gi += ADT / 32)
+            aq_dec_job(oq.L, out, oq.M, 0, oq.row_bits, oq.bits, oq.ws, oq.A, oq.err, 0, hh * gph + gi, e, centred);
+    }
+}
+
+// Decode-pass form of add_rmsnorm8_kernel with the next linear's activation
+// quantization in its epilogue.  CTA (row, slice): every CTA of a row reads
+// the whole row of h_in (+ delta) and forms the row's sum of squares exactly
+// as add_rmsnorm8_kernel does (same thread mapping, same reduction, so the
+// same bits), then writes only its d/NS slice of h_out (= h_in + delta, or a
+// copy) and y, and quantizes that slice's K-groups with aq_dec_job.  h_in is never written (the policy step
+// alternates two h buffers), so no CTA reads a value another CTA updated.
+__global__ void __launch_bounds__(1024) add_rmsnorm_q_kernel(const uint16_t* __restrict__ h_in,
+                                                             const uint16_t* __restrict__ delta,
+                                                             const uint16_t* __restrict__ w, int d, float eps,
+                                                             uint16_t* __restrict__ y, uint16_t* __restrict__ h_out,
+                                                             OQuant q) {
+    __shared__ float red[32];
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    const int row = blockIdx.x, slice = blockIdx.y, NS = gridDim.y;
+    const int tps = (int)blockDim.x / NS;  // threads per slice
+    const bool mine = (int)threadIdx.x / tps == slice;
+    const size_t o = (size_t)row * d + threadIdx.x * 8;
+    const uint4 hv = *reinterpret_cast<const uint4*>(h_in + o);
+    const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+    float a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = bf2f((uint16_t)(hw[k >> 1] >> (16 * (k & 1))));
+    uint32_t nh[4] = {hw[0], hw[1], hw[2], hw[3]};
+    if (delta) {
+        const uint4 dv = *reinterpret_cast<const uint4*>(delta + o);
+        const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            const uint16_t lo = f2bf(a[k] + bf2f((uint16_t)(dw[k >> 1] & 0xffffu)));
+            const uint16_t hi = f2bf(a[k + 1] + bf2f((uint16_t)(dw[k >> 1] >> 16)));
+            a[k] = bf2f(lo);
+            a[k + 1] = bf2f(hi);
+            nh[k >> 1] = (uint32_t)lo | ((uint32_t)hi << 16);
         }
     }
+    if (mine && h_out) *reinterpret_cast<uint4*>(h_out + o) = make_uint4(nh[0], nh[1], nh[2], nh[3]);
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) ss += a[k] * a[k] + a[k + 1] * a[k + 1];
+    const float inv = rsqrtf(block_sum(ss, red) / (float)d + eps);
+    if (mine) {
+        const uint4 wv = *reinterpret_cast<const uint4*>(w + threadIdx.x * 8);
+        const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+        uint32_t yo[4];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            const uint16_t lo = f2bf(a[k] * inv * bf2f((uint16_t)(ww[k >> 1] & 0xffffu)));
+            const uint16_t hi = f2bf(a[k + 1] * inv * bf2f((uint16_t)(ww[k >> 1] >> 16)));
+            yo[k >> 1] = (uint32_t)lo | ((uint32_t)hi << 16);
+        }
+        *reinterpret_cast<uint4*>(y + o) = make_uint4(yo[0], yo[1], yo[2], yo[3]);
+    }
+    if (!q.ws) return;
+    __syncthreads();  // this CTA's slice of y is written (CTA-visible)
+    // (the padding rows M .. 8 nt8 - 1 of the records are left as they are:
+    // the decode kernel's token columns are independent, padding columns are
+    // never stored)
+    const int G = q.L.G, gps = d / NS / G;
+    const bool centred = dec_call_centred(q.M, 0, q.row_bits, q.bits);
+    for (int gi = (int)threadIdx.x >> 5; gi < gps; gi += (int)blockDim.x >> 5)
+        aq_dec_job(q.L, y, q.M, 0, q.row_bits, q.bits, q.ws, q.A, q.err, 0, slice * gps + gi, row, centred);
 }
 
 __global__ void silu_mul_kernel(const uint16_t* __restrict__ gu, int M, int ffn, uint16_t* __restrict__ act) {
@@ -858,7 +920,7 @@ static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct ModelLayout {
     int S, T, MP;
-    size_t h, xn, delta, att, qkv, gu, act, ws[8], rbp, rbd, bits, tok, prev, logits, err, total;
+    size_t h, h2, xn, delta, att, qkv, gu, act, ws[8], rbp, rbd, bits, tok, prev, logits, err, total;
     size_t rb8p, rb8d, gates;      // variant table: W8 rows (prefill / decode), gates [W4p, W8p, W4d, W8d]
     size_t ws_bytes[8], kv_bytes;  // one qlinear workspace per linear shape (split-K counters are per shape); 4-7: W8
     bool w8;
@@ -925,6 +987,7 @@ static dyq_status_t model_layout(const dyq_model_desc_t* m, ModelLayout* L) {
     size_t o = 0;
     auto take = [&](size_t bytes) { const size_t r = o; o += al256(bytes); return r; };
     L->h = take(MP * d * 2);
+    L->h2 = take(MP * d * 2);  // the decode passes' second h buffer (add_rmsnorm_q ping-pong)
     L->xn = take(MP * d * 2);
     L->delta = take(MP * d * 2);
     L->att = take(MP * d * 2);
@@ -1050,6 +1113,19 @@ static dyq_status_t attention_decode(const uint16_t* qkv, int32_t E, int32_t pos
     const size_t smem = (HD + (size_t)(pos + 1) + 32 + 4 * HD) * 4;
     attn_decode_kernel<<<dim3(H, E), 256, smem, stream>>>(qkv, pos, d, H, kv, layer, L, T, out);
     return check_launch("attn_decode_kernel");
+}
+
+// add_rmsnorm_q_kernel launcher: DYQ_EUNSUPPORTED (nothing launched) when the
+// shape does not split into 256-wide slices of whole K-groups.
+static dyq_status_t add_rmsnorm_q(const uint16_t* h_in, const uint16_t* delta, const uint16_t* w, int M, int d,
+                                  float eps, uint16_t* y, uint16_t* h_out, const OQuant& q, cudaStream_t st) {
+    if (M <= 0 || d % 256 || d / 8 > 1024 || (q.ws && (256 % q.L.G || q.L.K != d))) return DYQ_EUNSUPPORTED;
+    if (((uintptr_t)h_in | (uintptr_t)delta | (uintptr_t)w | (uintptr_t)y | (uintptr_t)h_out) % 16)
+        return DYQ_EUNSUPPORTED;
+    const cudaError_t e = launch_pdl(add_rmsnorm_q_kernel, dim3(M, d / 256), dim3(d / 8), 0, st, h_in, delta, w, d,
+                                     eps, y, h_out, q);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "add_rmsnorm_q_kernel: %s", cudaGetErrorString(e));
+    return check_launch("add_rmsnorm_q_kernel");
 }
 }  // namespace dyq
 
@@ -1287,10 +1363,56 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
         return rc;
     };
 
+    // Decode passes, W4-pinned table, M <= 16: the activation quantization of
+    // the o, gate|up and next-layer qkv projections runs in the epilogue of
+    // the kernel producing their input (attention, add + RMSNorm), each
+    // linear then runs dyq_qlinear_q on those records.  add_rmsnorm_q reads
+    // h from hc and writes h + delta to ho (then swapped), two per layer, so
+    // hc is h again at the end of every pass.
+    uint16_t* hc = h;
+    uint16_t* ho = m->at<uint16_t>(L.h2);
+    bool qkv_ready = false;  // xn's qkv records already in ws[0]
+    auto oquant = [&](int which, int M, int32_t* rb) {
+        OQuant q{};
+        WLayout Lw;
+        if (make_layout(&wd[which], &Lw)) {
+            q.ws = dec_act_area(Lw, ws[which]);
+            q.A = act_layout_dec(Lw, dec_nt8(M));
+            q.L = Lw;
+            q.row_bits = rb;
+            q.bits = 0;
+            q.M = M;
+            q.err = err;
+        }
+        return q;
+    };
+    // add + RMSNorm into xn; quantizes xn for linear `which` (-1: none) when
+    // fusable; returns whether the records were written
+    auto norm = [&](const uint16_t* dl, const uint16_t* nwt, int M, int32_t* rb, int which, bool fusable,
+                    bool* quantized) -> dyq_status_t {
+        *quantized = false;
+        if (fusable) {
+            const OQuant q = which >= 0 ? oquant(which, M, rb) : OQuant{};
+            const dyq_status_t r = add_rmsnorm_q(hc, dl, nwt, M, d, D.rms_eps, xn, dl ? ho : nullptr, q, st);
+            if (r == DYQ_OK) {
+                if (dl) std::swap(hc, ho);
+                *quantized = q.ws != nullptr;
+                return DYQ_OK;
+            }
+            if (r != DYQ_EUNSUPPORTED) return r;
+        }
+        return dyq_add_rmsnorm(hc, dl, nwt, M, d, D.rms_eps, xn, stream);
+    };
     auto layer = [&](int l, int M, int32_t* rb, int32_t* rb8, const int32_t* g, bool prefill, int pos)
         -> dyq_status_t {
         const size_t li = (size_t)4 * l;
-        DYQ_TRY(qlin(0, li, xn, M, rb, rb8, g, qkv, false));
+        const bool fuse = fuse_oq && !prefill && !(w8 && rb8 != nullptr) && M <= DEC_MPAD;
+        if (qkv_ready && fuse)
+            DYQ_TRY(dyq_qlinear_q(&wd[0], m->codes[li], m->meta[li], xn, M, rb, 0, qkv, 1, ws[0], L.ws_bytes[0],
+                                  stream));
+        else
+            DYQ_TRY(qlin(0, li, xn, M, rb, rb8, g, qkv, false));
+        qkv_ready = false;
         bool o_done = false;
         if (prefill) {
             DYQ_TRY(dyq_rope(qkv, M, S, 0, d, H, D.rope_theta, stream));
@@ -1327,13 +1449,18 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
                                   L.ws_bytes[1], stream));
         else
             DYQ_TRY(qlin(1, li, att, M, rb, rb8, g, delta, false));
-        DYQ_TRY(dyq_add_rmsnorm(h, delta, D.mlp_norm + (size_t)l * d, M, d, D.rms_eps, xn, stream));
-        DYQ_TRY(qlin(2, li, xn, M, rb, rb8, g, gu, false));
+        bool gu_ready = false;
+        DYQ_TRY(norm(delta, D.mlp_norm + (size_t)l * d, M, rb, 2, fuse, &gu_ready));
+        if (gu_ready)
+            DYQ_TRY(dyq_qlinear_q(&wd[2], m->codes[li + 2], m->meta[li + 2], xn, M, rb, 0, gu, 1, ws[2],
+                                  L.ws_bytes[2], stream));
+        else
+            DYQ_TRY(qlin(2, li, xn, M, rb, rb8, g, gu, false));
         // SwiGLU fused into the down projection's activation quantization
         // (bit-identical to dyq_silu_mul + dyq_qlinear; one launch less per layer)
         DYQ_TRY(qlin(3, li, gu, M, rb, rb8, g, delta, true));
         const uint16_t* nw = l + 1 < NL ? D.attn_norm + (size_t)(l + 1) * d : D.final_norm;
-        DYQ_TRY(dyq_add_rmsnorm(h, delta, nw, M, d, D.rms_eps, xn, stream));
+        DYQ_TRY(norm(delta, nw, M, rb, l + 1 < NL ? 0 : -1, fuse, &qkv_ready));
         return DYQ_OK;
     };
 
@@ -1353,8 +1480,14 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
                        d, h) != cudaSuccess)
             return set_error(DYQ_ECUDA, "embed_action_kernel launch");
         DYQ_TRY(check_launch("embed_action_kernel"));
-        DYQ_TRY(dyq_add_rmsnorm(h, nullptr, D.attn_norm, E, d, D.rms_eps, xn, stream));
+        DYQ_TRY(norm(nullptr, D.attn_norm, E, rbd, 0, fuse_oq && !(w8 && rb8d != nullptr) && E <= DEC_MPAD,
+                     &qkv_ready));
         for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, E, rbd, rb8d, gates + 2, false, S + t - 1));
+        if (hc != h) {  // odd number of in-place fallbacks: bring h home
+            if (cudaMemcpyAsync(h, hc, (size_t)E * d * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return check_launch("h copy");
+            std::swap(hc, ho);
+        }
         DYQ_TRY(dyq_head_argmax(xn, E, 1, d, D.head_bins, D.n_bins, logits, tok + t, D.n_act, stream));
     }
     if (launch_pdl(detok_kernel, dim3((E * D.n_act + 127) / 128), dim3(128), 0, st, tok, E, D.n_act, D.n_bins,

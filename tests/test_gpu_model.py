@@ -217,9 +217,11 @@ def test_policy_step_matches_reference_and_selector():
 @pytest.mark.parametrize("E", [1, 3])
 def test_policy_step_fused_o_quant_is_bit_identical(E, monkeypatch):
     """The decode passes quantize the o projection's input in the attention
-    kernel's epilogue (aq_dec_job, the standalone quantizer's own code); with
-    DYQ_FUSE_OQ=0 the separate act-quant kernel runs.  Same actions, bits and
-    KV cache either way."""
+    kernel's epilogue and the gate|up / next-layer qkv inputs in the add +
+    RMSNorm kernel's epilogue (aq_dec_job, the standalone quantizer's own
+    code; add_rmsnorm_q with the same row reduction as add_rmsnorm8); with
+    DYQ_FUSE_OQ=0 the separate kernels run.  Same actions, bits and KV cache
+    either way."""
     n_vis, n_text = 8, 4
     w = _tiny(5)
     cal = dyq.default_calib()
