@@ -274,6 +274,11 @@ extern "C" {
 static size_t prefill_area_offset(const WLayout& L) {
     return ((act_area_offset(L) + act_layout_dec(L, 2).bytes + 1023) & ~(size_t)1023) + PRE_CNT_BYTES;
 }
+}  // extern "C"
+namespace dyq {
+uint8_t* pre_act_area(const WLayout& L, void* ws) { return reinterpret_cast<uint8_t*>(ws) + prefill_area_offset(L); }
+}  // namespace dyq
+extern "C" {
 
 dyq_status_t dyq_qlinear_workspace(const dyq_wdesc_t* wd, int32_t M, size_t* bytes) {
     WLayout L;

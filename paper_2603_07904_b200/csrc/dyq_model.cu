@@ -59,10 +59,22 @@ __global__ void add_rmsnorm_kernel(uint16_t* __restrict__ h, const uint16_t* __r
 
 // Same op, one 16-B vector of 8 elements per thread (d = 8 * blockDim.x), h
 // kept in registers between the statistics and the output pass; PDL-launched.
+// Prefill activation records of the next linear written by add_rmsnorm8's
+// epilogue (policy step prefill pass): act = the linear's prefill activation
+// area (null: off), rows 0 .. M-1.
+struct PQuant {
+    uint8_t* act;
+    PreActLayout P;
+    WLayout L;
+    const int32_t* row_bits;
+    int bits, M;
+    int64_t* err;
+};
+
 __global__ void __launch_bounds__(1024) add_rmsnorm8_kernel(uint16_t* __restrict__ h,
                                                             const uint16_t* __restrict__ delta,
                                                             const uint16_t* __restrict__ w, int d, float eps,
-                                                            uint16_t* __restrict__ y) {
+                                                            uint16_t* __restrict__ y, PQuant pq) {
     __shared__ float red[32];
     ptx::pdl_wait();
     ptx::pdl_launch_dependents();
@@ -100,6 +112,21 @@ __global__ void __launch_bounds__(1024) add_rmsnorm8_kernel(uint16_t* __restrict
         yo[k >> 1] = (uint32_t)lo | ((uint32_t)hi << 16);
     }
     *reinterpret_cast<uint4*>(y + o) = make_uint4(yo[0], yo[1], yo[2], yo[3]);
+    if (!pq.act) return;
+    // the row's records: thread (g, quarter) = one aqp_job (NG * 4 threads,
+    // whole warps; bf16 operand mode), and the token tile's mode byte
+    __syncthreads();  // the row of y is written (CTA-visible)
+    const int row = blockIdx.x, tt = row / PRE_PT;
+    const int t = (int)threadIdx.x;
+    if (t < pq.L.NG * AQP_TPR) {
+        if (pq.L.G == 64)
+            aqp_job<16>(pq.L, y, pq.M, pq.row_bits, pq.bits, pq.act, pq.P, pq.err, false, 0, tt, t / AQP_TPR,
+                        row - tt * PRE_PT, t % AQP_TPR);
+        else
+            aqp_job<32>(pq.L, y, pq.M, pq.row_bits, pq.bits, pq.act, pq.P, pq.err, false, 0, tt, t / AQP_TPR,
+                        row - tt * PRE_PT, t % AQP_TPR);
+    }
+    if (t == 0 && row == tt * PRE_PT) pq.act[pq.P.mode_off + tt] = 0;  // bf16 operands
 }
 
 // Launch with programmatic dependent launch (every kernel launched this way
@@ -1036,7 +1063,7 @@ dyq_status_t dyq_add_rmsnorm(uint16_t* h, const uint16_t* delta, const uint16_t*
     const bool al = ((uintptr_t)h | (uintptr_t)w | (uintptr_t)y | (uintptr_t)delta) % 16 == 0;
     if (d % 256 == 0 && d / 8 <= 1024 && al) {
         const cudaError_t e = launch_pdl(add_rmsnorm8_kernel, dim3(M), dim3(d / 8), 0, (cudaStream_t)stream, h, delta,
-                                         w, d, eps, y);
+                                         w, d, eps, y, PQuant{});
         if (e != cudaSuccess) return set_error(DYQ_ECUDA, "add_rmsnorm8_kernel: %s", cudaGetErrorString(e));
         return check_launch("add_rmsnorm8_kernel");
     }
@@ -1126,6 +1153,21 @@ static dyq_status_t add_rmsnorm_q(const uint16_t* h_in, const uint16_t* delta, c
                                      eps, y, h_out, q);
     if (e != cudaSuccess) return set_error(DYQ_ECUDA, "add_rmsnorm_q_kernel: %s", cudaGetErrorString(e));
     return check_launch("add_rmsnorm_q_kernel");
+}
+
+// add_rmsnorm8_kernel with the next linear's prefill records in its epilogue;
+// DYQ_EUNSUPPORTED (nothing launched) when a row's K-groups are not whole
+// warps of quarter jobs or the shape / alignment does not fit the kernel.
+static dyq_status_t add_rmsnorm_pq(uint16_t* h, const uint16_t* delta, const uint16_t* w, int M, int d, float eps,
+                                   uint16_t* y, const PQuant& pq, cudaStream_t st) {
+    const int jobs = pq.L.NG * AQP_TPR;
+    if (M <= 0 || d % 256 || d / 8 > 1024 || pq.L.K != d || (pq.L.G != 64 && pq.L.G != 128) || jobs > d / 8 ||
+        jobs % 32)
+        return DYQ_EUNSUPPORTED;
+    if (((uintptr_t)h | (uintptr_t)delta | (uintptr_t)w | (uintptr_t)y) % 16) return DYQ_EUNSUPPORTED;
+    const cudaError_t e = launch_pdl(add_rmsnorm8_kernel, dim3(M), dim3(d / 8), 0, st, h, delta, w, d, eps, y, pq);
+    if (e != cudaSuccess) return set_error(DYQ_ECUDA, "add_rmsnorm8_kernel: %s", cudaGetErrorString(e));
+    return check_launch("add_rmsnorm8_kernel");
 }
 }  // namespace dyq
 
@@ -1386,12 +1428,36 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
         }
         return q;
     };
-    // add + RMSNorm into xn; quantizes xn for linear `which` (-1: none) when
-    // fusable; returns whether the records were written
-    auto norm = [&](const uint16_t* dl, const uint16_t* nwt, int M, int32_t* rb, int which, bool fusable,
+    auto pquant = [&](int which, int M, int32_t* rb) {
+        PQuant q{};
+        WLayout Lw;
+        if (make_layout(&wd[which], &Lw) && !prefill_e4m3(Lw)) {
+            q.act = pre_act_area(Lw, ws[which]);
+            q.P = pre_act_layout(Lw, M);
+            q.L = Lw;
+            q.row_bits = rb;
+            q.bits = 0;
+            q.M = M;
+            q.err = err;
+        }
+        return q;
+    };
+    // add + RMSNorm into xn; with mode 1 (decode path) / 2 (prefill path) it
+    // also writes linear `which`'s activation records (-1: none); *quantized
+    // tells whether it did
+    auto norm = [&](const uint16_t* dl, const uint16_t* nwt, int M, int32_t* rb, int which, int mode,
                     bool* quantized) -> dyq_status_t {
         *quantized = false;
-        if (fusable) {
+        if (mode == 2 && which >= 0) {
+            const PQuant q = pquant(which, M, rb);
+            const dyq_status_t r = q.act ? add_rmsnorm_pq(hc, dl, nwt, M, d, D.rms_eps, xn, q, st) : DYQ_EUNSUPPORTED;
+            if (r == DYQ_OK) {
+                *quantized = true;
+                return DYQ_OK;
+            }
+            if (r != DYQ_EUNSUPPORTED) return r;
+        }
+        if (mode == 1) {
             const OQuant q = which >= 0 ? oquant(which, M, rb) : OQuant{};
             const dyq_status_t r = add_rmsnorm_q(hc, dl, nwt, M, d, D.rms_eps, xn, dl ? ho : nullptr, q, st);
             if (r == DYQ_OK) {
@@ -1403,13 +1469,29 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
         }
         return dyq_add_rmsnorm(hc, dl, nwt, M, d, D.rms_eps, xn, stream);
     };
+    // the fused records' mode for an M-row call: 1 = decode kernels (M <= 16),
+    // 2 = prefill kernels, as dyq_qlinear would route it; 0 = separate kernels
+    auto fuse_mode = [&](int M, int32_t* rb8) {
+        if (!fuse_oq || (w8 && rb8 != nullptr) || g_path != 0) return 0;
+        return M <= DEC_MPAD ? 1 : 2;
+    };
+    // linear `which` on the records its producer wrote (mode 1 / 2)
+    auto run_ready = [&](int which, size_t li, const uint16_t* x, int M, int32_t* rb, uint16_t* y,
+                         int mode) -> dyq_status_t {
+        if (mode == 1)
+            return dyq_qlinear_q(&wd[which], m->codes[li + which], m->meta[li + which], x, M, rb, 0, y, 1, ws[which],
+                                 L.ws_bytes[which], stream);
+        WLayout Lw;
+        if (!make_layout(&wd[which], &Lw)) return set_error(DYQ_EINVAL, "bad weight descriptor");
+        return launch_prefill(Lw, m->codes[li + which], m->meta[li + which], M, rb, 0, y, 1, nullptr,
+                              pre_act_area(Lw, ws[which]), st);
+    };
     auto layer = [&](int l, int M, int32_t* rb, int32_t* rb8, const int32_t* g, bool prefill, int pos)
         -> dyq_status_t {
         const size_t li = (size_t)4 * l;
-        const bool fuse = fuse_oq && !prefill && !(w8 && rb8 != nullptr) && M <= DEC_MPAD;
-        if (qkv_ready && fuse)
-            DYQ_TRY(dyq_qlinear_q(&wd[0], m->codes[li], m->meta[li], xn, M, rb, 0, qkv, 1, ws[0], L.ws_bytes[0],
-                                  stream));
+        const int fmode = fuse_mode(M, rb8);
+        if (qkv_ready && fmode)
+            DYQ_TRY(run_ready(0, li, xn, M, rb, qkv, fmode));
         else
             DYQ_TRY(qlin(0, li, xn, M, rb, rb8, g, qkv, false));
         qkv_ready = false;
@@ -1450,17 +1532,24 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
         else
             DYQ_TRY(qlin(1, li, att, M, rb, rb8, g, delta, false));
         bool gu_ready = false;
-        DYQ_TRY(norm(delta, D.mlp_norm + (size_t)l * d, M, rb, 2, fuse, &gu_ready));
+        DYQ_TRY(norm(delta, D.mlp_norm + (size_t)l * d, M, rb, 2, fmode, &gu_ready));
         if (gu_ready)
-            DYQ_TRY(dyq_qlinear_q(&wd[2], m->codes[li + 2], m->meta[li + 2], xn, M, rb, 0, gu, 1, ws[2],
-                                  L.ws_bytes[2], stream));
+            DYQ_TRY(run_ready(2, li, xn, M, rb, gu, fmode));
         else
             DYQ_TRY(qlin(2, li, xn, M, rb, rb8, g, gu, false));
         // SwiGLU fused into the down projection's activation quantization
         // (bit-identical to dyq_silu_mul + dyq_qlinear; one launch less per layer)
         DYQ_TRY(qlin(3, li, gu, M, rb, rb8, g, delta, true));
         const uint16_t* nw = l + 1 < NL ? D.attn_norm + (size_t)(l + 1) * d : D.final_norm;
-        DYQ_TRY(norm(delta, nw, M, rb, l + 1 < NL ? 0 : -1, fuse, &qkv_ready));
+        DYQ_TRY(norm(delta, nw, M, rb, l + 1 < NL ? 0 : -1, fmode, &qkv_ready));
+        return DYQ_OK;
+    };
+    auto bring_h_home = [&]() -> dyq_status_t {  // after an odd number of in-place fallbacks
+        if (hc != h) {
+            if (cudaMemcpyAsync(h, hc, (size_t)L.MP * d * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return check_launch("h copy");
+            std::swap(hc, ho);
+        }
         return DYQ_OK;
     };
 
@@ -1470,8 +1559,9 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
         cudaSuccess)
         return set_error(DYQ_ECUDA, "embed_prefill_kernel launch");
     DYQ_TRY(check_launch("embed_prefill_kernel"));
-    DYQ_TRY(dyq_add_rmsnorm(h, nullptr, D.attn_norm, MP, d, D.rms_eps, xn, stream));
+    DYQ_TRY(norm(nullptr, D.attn_norm, MP, rbp, 0, fuse_mode(MP, paper ? nullptr : rb8p), &qkv_ready));
     for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, MP, rbp, paper ? nullptr : rb8p, gates, true, 0));
+    DYQ_TRY(bring_h_home());
     if (paper && cudaStreamWaitEvent(st, m->ev_join, 0) != cudaSuccess) return check_launch("paper-mode join");
     DYQ_TRY(dyq_head_argmax(xn + (size_t)(S - 1) * d, E, S, d, D.head_bins, D.n_bins, logits, tok, D.n_act, stream));
     // ---- decode passes: one action token per pass
@@ -1480,14 +1570,9 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
                        d, h) != cudaSuccess)
             return set_error(DYQ_ECUDA, "embed_action_kernel launch");
         DYQ_TRY(check_launch("embed_action_kernel"));
-        DYQ_TRY(norm(nullptr, D.attn_norm, E, rbd, 0, fuse_oq && !(w8 && rb8d != nullptr) && E <= DEC_MPAD,
-                     &qkv_ready));
+        DYQ_TRY(norm(nullptr, D.attn_norm, E, rbd, 0, fuse_mode(E, rb8d), &qkv_ready));
         for (int l = 0; l < NL; ++l) DYQ_TRY(layer(l, E, rbd, rb8d, gates + 2, false, S + t - 1));
-        if (hc != h) {  // odd number of in-place fallbacks: bring h home
-            if (cudaMemcpyAsync(h, hc, (size_t)E * d * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-                return check_launch("h copy");
-            std::swap(hc, ho);
-        }
+        DYQ_TRY(bring_h_home());
         DYQ_TRY(dyq_head_argmax(xn, E, 1, d, D.head_bins, D.n_bins, logits, tok + t, D.n_act, stream));
     }
     if (launch_pdl(detok_kernel, dim3((E * D.n_act + 127) / 128), dim3(128), 0, st, tok, E, D.n_act, D.n_bins,

@@ -70,7 +70,7 @@ static_assert(PT == PRE_PT, "dyq_tp_flag_delta counts prefill token tiles");
 // sub-partition holds 16 K, so > 12 warps per CTA cap a thread at 128.)
 constexpr int PRE_WARPS = 15;
 constexpr int PRE_THREADS = PRE_WARPS * 32;
-constexpr int PAR_BYTES = PT * 4;  // per (tile, group): float s_x[144] (1 for A16 tokens, 0 for absent)
+constexpr int PAR_BYTES = PRE_PAR_BYTES;  // per (tile, group): float s_x[144] (1 for A16 tokens, 0 for absent)
 constexpr int XF_WARP0 = 3, XF_WARPS = 4;
 constexpr int PR_WARP0 = 7, PR_WARPS = 8;  // promotion warps
 constexpr int STG_ROW = 128 * 2 + 16;  // epilogue staging: bytes per token (128 bf16 rows + pad)
@@ -131,10 +131,8 @@ struct PreArgs {
 // Physical byte position, inside one 32-k e4m3 K step, of logical k (0..31):
 // the packed W4 fragment puts k = 4t + i (low nibbles) in TMEM column 2t and
 // k = 16 + 4t + i (high nibbles) in column 2t + 1, so B follows that order.
-__host__ __device__ inline int e4m3_kpos(int kl) { return 8 * ((kl >> 2) & 3) + 4 * ((kl >> 4) & 1) + (kl & 3); }
-__device__ __forceinline__ uint8_t e4m3_of(float v) {  // exact for integers |v| <= 15
-    return (uint8_t)__nv_cvt_float_to_fp8(v, __NV_SATFINITE, __NV_E4M3);
-}
+
+
 
 // Stream-K partition: CTA c owns work groups [sk_begin(c), sk_begin(c + 1)) of
 // the flat order w = ((tile * TT + tt) * NG + g) -- tile-major, so the token
@@ -660,7 +658,6 @@ __global__ void __launch_bounds__(PRE_THREADS, 1) qlinear_prefill_kernel(const P
 // holding the centred codes Xq - z_x of Eq. (2) for integer tokens (exact in
 // bf16 / e4m3), x itself for A16 tokens and 0 for absent rows; and s_x per
 // token (1 for A16 tokens, 0 for absent rows) at the head of the record.
-constexpr int AQP_TPR = 4;  // threads per token row
 template <int KH>  // inputs per thread = G / AQP_TPR
 __global__ void __launch_bounds__(AQP_TPR * PT) actquant_pre_kernel(WLayout L, const uint16_t* __restrict__ x, int M,
                                                           const int32_t* __restrict__ row_bits, int bits,
@@ -669,136 +666,15 @@ __global__ void __launch_bounds__(AQP_TPR * PT) actquant_pre_kernel(WLayout L, c
     if (gate_closed(gate)) return;
     ptx::pdl_wait();  // x / row_bits come from the preceding kernels
     ptx::pdl_launch_dependents();
-    const int NG = L.NG, G = L.G;
+    const int NG = L.NG;
     const int g = blockIdx.x % NG, tt = blockIdx.x / NG;
     const int row = threadIdx.x / AQP_TPR, half = threadIdx.x % AQP_TPR;  // half: quarter of the group
     const int m = tt * PT + row;
     const int b = m < M ? (row_bits ? row_bits[m] : bits) : 0;
     // tile mode (dyq_pre_tile_e4m3): every present token of tile tt at A2 / A4
     const bool f8 = e4m3_ok && __syncthreads_and(m >= M || b == 2 || b == 4);
-    const size_t tg = (size_t)tt * NG + g;
     if (threadIdx.x == 0 && g == 0) act[P.mode_off + tt] = f8 ? 1 : 0;  // read by the MMA kernel
-    uint8_t* xg = act + tg * P.rec + PAR_BYTES;  // record [s_x | B]
-    const int k0 = half * KH;  // inputs k0 .. k0 + KH - 1
-    const uint16_t* src = x + (size_t)(m < M ? m : 0) * L.K * (gated ? 2 : 1) + (size_t)g * G + k0;  // gated: [g | u]
-    constexpr int NW = KH / 2;  // 32-bit words per thread
-    uint32_t raw[NW];
-    float vmin = 0.f, vmax = 0.f;
-    int bad = 0x7fffffff;
-    if (b != 0) {
-#pragma unroll
-        for (int i = 0; i < NW; i += 4) {
-            uint4 w4 = *reinterpret_cast<const uint4*>(src + 2 * i);
-            if (gated) {
-                const uint4 u4 = *reinterpret_cast<const uint4*>(src + L.K + 2 * i);
-                const uint32_t gw[4] = {w4.x, w4.y, w4.z, w4.w}, uw[4] = {u4.x, u4.y, u4.z, u4.w};
-                uint32_t o[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    o[e] = (uint32_t)silu_mul_bf16(gw[e] & 0xffffu, uw[e] & 0xffffu) |
-                           ((uint32_t)silu_mul_bf16(gw[e] >> 16, uw[e] >> 16) << 16);
-                w4 = make_uint4(o[0], o[1], o[2], o[3]);
-            }
-            raw[i] = w4.x;
-            raw[i + 1] = w4.y;
-            raw[i + 2] = w4.z;
-            raw[i + 3] = w4.w;
-        }
-#pragma unroll
-        for (int i = 0; i < NW; ++i)
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const float v = bf16_bits_to_float((uint16_t)(raw[i] >> (16 * hh)));
-                if (!finite_f(v)) bad = min(bad, k0 + 2 * i + hh);
-                vmin = fminf(vmin, v);
-                vmax = fmaxf(vmax, v);
-            }
-    }
-    // quad combine (the row's four threads are adjacent lanes)
-    vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, 1));
-    vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, 1));
-    bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, 1));
-    vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, 2));
-    vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, 2));
-    bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, 2));
-    if (bad != 0x7fffffff && half == 0) report_nonfinite(err, (int64_t)m * L.K + (int64_t)g * G + bad);
-    float* sxo = reinterpret_cast<float*>(act + tg * P.rec) + row;
-    const bool quant = b == 2 || b == 4 || b == 8;
-    float s = 1.f;
-    int z = 0;
-    if (quant) fit_params(vmin, vmax, b, &s, &z);
-    if (half == 0) *sxo = quant ? s : (b == 16 ? 1.f : 0.f);
-    // codes of this thread's inputs (as exact centred integers), then the
-    // layout-ordered 16-B stores
-    auto val = [&](int i, int hh) -> float {  // input k0 + 2i + hh
-        const uint16_t r = (uint16_t)(raw[i] >> (16 * hh));
-        if (quant) return (float)(quantize_one(bf16_bits_to_float(r), s, z, b, L.round_mode) - z);
-        return 0.f;
-    };
-    uint8_t* rowb = xg + (row >> 3) * 256 + (row & 7) * 16;
-    if (!f8) {
-        // bf16: this thread covers K steps ks = k0/16 .. (k0 + KH)/16 - 1
-#pragma unroll
-        for (int ks = 0; ks < KH / 16; ++ks) {
-#pragma unroll
-            for (int kh = 0; kh < 2; ++kh) {  // kk >> 3
-                uint32_t o[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int i = ks * 8 + kh * 4 + e;  // word index: k = k0 + 2i, 2i + 1
-                    if (b == 16) {
-                        o[e] = raw[i];
-                    } else if (quant) {
-                        const __nv_bfloat162 p2 = __floats2bfloat162_rn(val(i, 0), val(i, 1));  // |q - z| <= 255: exact
-                        o[e] = *reinterpret_cast<const uint32_t*>(&p2);
-                    } else {
-                        o[e] = 0;
-                    }
-                }
-                const int KS = (k0 >> 4) + ks;
-                *reinterpret_cast<uint4*>(rowb + KS * (PT * 32) + kh * 128) = make_uint4(o[0], o[1], o[2], o[3]);
-            }
-        }
-    } else if constexpr (KH == 16) {
-        // e4m3, G = 64: a 32-k K step spans thread pair (A: k 0-15, B: 16-31);
-        // chunk 0 = [A0 B0 A1 B1], chunk 1 = [A2 B2 A3 B3] (4-byte runs of k)
-        uint32_t w[4];
-#pragma unroll
-        for (int r4 = 0; r4 < 4; ++r4) {
-            w[r4] = 0u;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int kt = 4 * r4 + e;
-                const uint32_t q8 = quant ? (uint32_t)e4m3_of(val(kt >> 1, kt & 1)) : 0u;  // |q - z| <= 15
-                w[r4] |= q8 << (8 * e);
-            }
-        }
-        const bool isA = (half & 1) == 0;
-        const uint32_t x0 = __shfl_xor_sync(0xffffffffu, isA ? w[2] : w[0], 1);
-        const uint32_t x1 = __shfl_xor_sync(0xffffffffu, isA ? w[3] : w[1], 1);
-        const int KS = half >> 1;
-        const uint4 o = isA ? make_uint4(w[0], x0, w[1], x1) : make_uint4(x0, w[2], x1, w[3]);
-        *reinterpret_cast<uint4*>(rowb + KS * (PT * 32) + (isA ? 0 : 128)) = o;
-    } else {
-        // e4m3: one 32-k K step per thread (G = 128)
-#pragma unroll
-        for (int ks = 0; ks < KH / 32; ++ks) {
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {  // p >> 4
-                uint32_t o[4] = {0, 0, 0, 0};
-#pragma unroll
-                for (int pp = 0; pp < 16; ++pp) {
-                    const int p = 16 * c + pp;
-                    const int kl = (((p >> 2) & 1) << 4) | (((p >> 3) & 3) << 2) | (p & 3);  // e4m3_kpos^-1
-                    const int kt = ks * 32 + kl;  // input index within this thread
-                    const uint32_t q8 = quant ? (uint32_t)e4m3_of(val(kt >> 1, kt & 1)) : 0u;  // |q - z| <= 15
-                    o[pp >> 2] |= q8 << (8 * (pp & 3));
-                }
-                const int KS = (k0 >> 5) + ks;
-                *reinterpret_cast<uint4*>(rowb + KS * (PT * 32) + c * 128) = make_uint4(o[0], o[1], o[2], o[3]);
-            }
-        }
-    }
+    aqp_job<KH>(L, x, M, row_bits, bits, act, P, err, f8, gated, tt, g, row, half);
 }
 
 // ------------------------------------------------------------------ host
@@ -811,6 +687,8 @@ static bool pre_e4m3_enabled(const WLayout& L) {
     const char* v = getenv("DYQ_PRE_E4M3");
     return v && atoi(v) != 0 && L.wbits == 4;
 }
+
+bool prefill_e4m3(const WLayout& L) { return pre_e4m3_enabled(L); }
 
 PreActLayout pre_act_layout(const WLayout& L, int M) {
     PreActLayout P;

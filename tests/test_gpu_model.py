@@ -146,9 +146,9 @@ def test_silu_mul_and_head():
 
 
 # ------------------------------------------------------------------ whole step
-def _tiny(seed=0):
+def _tiny(seed=0, d=256):
     rng = np.random.default_rng(seed)
-    L, d, ffn, V, nb = 2, 256, 512, 512, 256
+    L, ffn, V, nb = 2, 2 * d, 512, 256
     shapes = [(3 * d, d), (d, d), (2 * ffn, d), (d, ffn)]
     w = {"lin": [[synth.weights_bf16(N, K, seed=100 * l + i + seed) for i, (N, K) in enumerate(shapes)]
                  for l in range(L)],
@@ -162,8 +162,9 @@ def _tiny(seed=0):
 
 def _gpu_model(w, E, n_vis, n_text):
     layers = [[dyq.PackedLinear.from_bf16(t16(lin), group=64, wbits=4) for lin in layer] for layer in w["lin"]]
+    d = w["lin"][0][1].shape[0]
     return dyq.Model(layers, t16(w["attn_norm"]), t16(w["mlp_norm"]), t16(w["final_norm"]), t16(w["embed"]),
-                     t16(w["head"]), E=E, n_heads=2, n_vis=n_vis, n_text=n_text, n_act=7)
+                     t16(w["head"]), E=E, n_heads=d // 128, n_vis=n_vis, n_text=n_text, n_act=7)
 
 
 def _margins(logits):
@@ -214,16 +215,18 @@ def test_policy_step_matches_reference_and_selector():
     assert total - exact <= max(1, total // 50), (exact, total)
 
 
-@pytest.mark.parametrize("E", [1, 3])
-def test_policy_step_fused_o_quant_is_bit_identical(E, monkeypatch):
+@pytest.mark.parametrize("E,d", [(1, 256), (3, 256), (1, 512), (2, 512)])
+def test_policy_step_fused_o_quant_is_bit_identical(E, d, monkeypatch):
     """The decode passes quantize the o projection's input in the attention
     kernel's epilogue and the gate|up / next-layer qkv inputs in the add +
     RMSNorm kernel's epilogue (aq_dec_job, the standalone quantizer's own
     code; add_rmsnorm_q with the same row reduction as add_rmsnorm8); with
     DYQ_FUSE_OQ=0 the separate kernels run.  Same actions, bits and KV cache
-    either way."""
+    either way.  At d = 512 (8 K-groups per row: whole warps of quarter jobs)
+    and 12 E > 16 prefill rows the prefill pass's add + RMSNorm also writes
+    the prefill records of gate|up and the next qkv."""
     n_vis, n_text = 8, 4
-    w = _tiny(5)
+    w = _tiny(5, d)
     cal = dyq.default_calib()
     res = []
     for fuse in ("1", "0"):
@@ -236,7 +239,7 @@ def test_policy_step_fused_o_quant_is_bit_identical(E, monkeypatch):
         bits = torch.zeros(E, dtype=torch.int32, device=DEV)
         out = []
         for _ in range(12):
-            vis = glue.to_bf16_bits(rng.standard_normal((E, n_vis, 256)))
+            vis = glue.to_bf16_bits(rng.standard_normal((E, n_vis, d)))
             text = rng.integers(0, 256, (E, n_text)).astype(np.int32)
             model.step(state, E, t16(vis.reshape(E, -1)), torch.from_numpy(text).to(DEV), act, bits)
             out.append((act.cpu().numpy().copy(), bits.cpu().numpy().copy()))
