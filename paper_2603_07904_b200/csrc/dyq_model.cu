@@ -1506,7 +1506,7 @@ static dyq_status_t policy_step_impl(void* model, void* state, const int32_t* fo
             // the separate kernels where the fused ones cannot run
             OQuant oq{};
             WLayout Lo;
-            const bool fuse_o = fuse_oq && !(w8 && rb8 != nullptr) && M <= DEC_MPAD && make_layout(&wd[1], &Lo);
+            const bool fuse_o = fmode == 1 && make_layout(&wd[1], &Lo);  // dyq_qlinear would take the decode path
             if (fuse_o) {
                 oq.ws = dec_act_area(Lo, ws[1]);
                 oq.A = act_layout_dec(Lo, dec_nt8(M));
